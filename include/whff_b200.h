@@ -1,0 +1,250 @@
+/*
+ * whff_b200.h -- C ABI of the B200-native WHFF hot path (libwhff_b200.so).
+ *
+ * Drop-in boundary for the reference's kernel plugin contract
+ * (whff/backend.py:36-46: a module exposing NAME, gemv_kernel,
+ * encode_blocks, decode_blocks) and for the device-resident parts of the
+ * codec / GEMV API the reference implements in Python on top of it.
+ * Each entry point cites the reference interface it replaces
+ * (paths relative to /root/reference/pkg/src/whff/; K = _kernels.pyx).
+ *
+ * Conventions
+ *  - Plain pointers and sizes only.  "dev" pointers are CUDA device memory of
+ *    the calling thread's current device; "host" pointers are host memory.
+ *  - Every compute call is asynchronous on the caller's stream
+ *    (whff_stream_t == cudaStream_t, NULL = legacy default stream) unless
+ *    documented as synchronous, and returns a whff_status_t.
+ *  - Device-detected data errors (non-finite decoded values) are reported
+ *    through a caller-owned device word `status_dev` (uint64, initialise to
+ *    WHFF_STATUS_CLEAR); after the stream is synchronised a value other than
+ *    WHFF_STATUS_CLEAR is the smallest flat index of a non-finite value.
+ *  - Outputs and workspaces are caller-owned; no allocation happens on the
+ *    hot path (decode / decode_gemv / gemv / plan launch).  Stream objects and
+ *    plans own their device memory (allocated at create, freed at destroy).
+ *  - Thread-safe across distinct handles and streams (no global mutable
+ *    state apart from the thread-local last-error message).
+ *  - Status codes map 1:1 onto errors.py:
+ *      WHFF_ERR_DIMENSION -> DimensionError      WHFF_ERR_NONFINITE -> NonFiniteError
+ *      WHFF_ERR_CORRUPT   -> CorruptStreamError  WHFF_ERR_ARGUMENT  -> WhffError
+ *      WHFF_ERR_OVERFLOW  -> WhffError (codec.py:240-241)
+ *      WHFF_ERR_NOMEM     -> MemoryError (K:105,118,254)
+ *      WHFF_ERR_CUDA      -> RuntimeError (device failure)
+ */
+#ifndef WHFF_B200_H
+#define WHFF_B200_H
+
+#include <stddef.h>
+#include <stdint.h>
+
+#ifdef __cplusplus
+extern "C" {
+#endif
+
+#define WHFF_ABI_VERSION 1
+#define WHFF_STATUS_CLEAR UINT64_MAX
+
+typedef struct CUstream_st* whff_stream_t; /* == cudaStream_t */
+typedef struct whff_dstream* whff_dstream_t;
+typedef struct whff_gemv_plan* whff_gemv_plan_t;
+
+typedef enum whff_status {
+  WHFF_OK = 0,
+  WHFF_ERR_DIMENSION = 1,
+  WHFF_ERR_NONFINITE = 2,
+  WHFF_ERR_CORRUPT = 3,
+  WHFF_ERR_ARGUMENT = 4,
+  WHFF_ERR_OVERFLOW = 5,
+  WHFF_ERR_NOMEM = 6,
+  WHFF_ERR_CUDA = 7
+} whff_status_t;
+
+/* codec.py:35-37 */
+typedef enum whff_mode { WHFF_MODE_RATE = 0, WHFF_MODE_PRECISION = 1, WHFF_MODE_ACCURACY = 2 } whff_mode_t;
+/* mpgemv.py:20 POLICIES */
+typedef enum whff_policy { WHFF_POLICY_MIXED = 0, WHFF_POLICY_SINGLE = 1, WHFF_POLICY_DOUBLE = 2 } whff_policy_t;
+/* mpgemv.py:21 SHAPES, plus the B200-native deterministic blocked order */
+typedef enum whff_shape {
+  WHFF_SHAPE_SEQUENTIAL = 0, /* strict left-to-right, bit-exact with K:24-47   */
+  WHFF_SHAPE_FIXED_TREE = 1, /* fixed-fanout tree, bit-exact with K:50-77       */
+  WHFF_SHAPE_BLOCKED = 2     /* B200 fast path: fixed split + butterfly order   */
+} whff_shape_t;
+/* how the fused decode+GEMV evaluates a block */
+typedef enum whff_eval {
+  WHFF_EVAL_EXACT = 0, /* bit-exact decoded words x, binary32 products x*v    */
+  WHFF_EVAL_COEFF = 1  /* coefficient domain: y = G * sum 2^(e-26) Q (G^T v)  */
+} whff_eval_t;
+/* device index layout chosen at stream creation */
+typedef enum whff_index_kind {
+  WHFF_INDEX_IMPLICIT = 0, /* fixed rate, offsets b*16*bpv: no index bytes   */
+  WHFF_INDEX_COMPACT = 1,  /* u64 base per 32 blocks of a block-row + u16 len */
+  WHFF_INDEX_FULL = 2      /* u64 start + u16 len per block                   */
+} whff_index_kind_t;
+
+typedef struct whff_dstream_info {
+  int32_t mode;
+  int32_t index_kind;
+  double param;
+  uint64_t rows, cols, n_blocks;
+  uint64_t payload_bytes;  /* as uploaded (reference payload.size)            */
+  uint64_t total_bits;     /* exact for GPU-encoded streams, else payload bits*/
+  uint64_t index_bytes;    /* device index bytes read by a full decode        */
+  uint64_t device_bytes;   /* all device memory owned by the stream           */
+  int32_t planes_limit;
+  int32_t has_raw_flag;
+} whff_dstream_info_t;
+
+int whff_abi_version(void);
+const char* whff_status_string(whff_status_t s);
+/* thread-local detail message of the last failing call on this thread */
+const char* whff_last_error(void);
+
+/* ------------------------------------------------------------------ */
+/* Device-resident compressed streams                                  */
+/* ------------------------------------------------------------------ */
+
+/* Upload a reference stream (codec.py:71-91 CompressedStream, or the WHFZ
+ * file read by codec.py:412-450 load_stream) to `device`.  Validates like
+ * codec.py:347-356 (_validate_stream) and :335-344 (_segment_lengths) and
+ * builds the device index.  Synchronous.                                   */
+whff_status_t whff_dstream_create(int device, int mode, double param,
+                                  uint64_t rows, uint64_t cols,
+                                  const uint8_t* payload_host, uint64_t payload_bytes,
+                                  const uint64_t* block_index_host, uint64_t n_blocks,
+                                  whff_dstream_t* out);
+/* Segment-table stream for the plugin-level decode_blocks (K:371-408),
+ * whose caller supplies explicit offsets/seglens (codec.py:304-306, :327-330)
+ * rather than a full stream.  Shape is 4 x 4*n_blocks.  Synchronous.      */
+whff_status_t whff_dstream_create_segments(int device, const uint8_t* payload_host,
+                                           uint64_t payload_bytes, const uint64_t* offsets_host,
+                                           const uint64_t* seglens_host, uint64_t n_blocks,
+                                           int planes_limit, int has_raw_flag,
+                                           whff_dstream_t* out);
+whff_status_t whff_dstream_destroy(whff_dstream_t s);
+whff_status_t whff_dstream_get_info(whff_dstream_t s, whff_dstream_info_t* info);
+/* Copy payload (payload_bytes) and u64 block bit offsets (n_blocks) back to
+ * the host, e.g. for codec.py:388-402 save_stream.  Synchronous.           */
+whff_status_t whff_dstream_download(whff_dstream_t s, uint8_t* payload_host,
+                                    uint64_t* block_index_host);
+
+/* ------------------------------------------------------------------ */
+/* Codec: encode (codec.py:225-268 compress; K:228-283 encode_blocks)   */
+/* ------------------------------------------------------------------ */
+
+/* GPU compress of a row-major float32 device matrix (pitch lda elements)
+ * into a new device stream.  Synchronous on `stream`.  Input must be finite
+ * (codec.py:231-232 is checked by the caller via whff_find_nonfinite).     */
+whff_status_t whff_compress(const float* a_dev, uint64_t lda, uint64_t rows, uint64_t cols,
+                            int mode, double param, whff_stream_t stream,
+                            whff_dstream_t* out);
+
+/* Plugin-level encode_blocks (K:228-283) from per-block coefficient arrays.
+ * Pass 1: per-block bit offsets (offsets_dev, nb) and the total bit count. */
+whff_status_t whff_encode_blocks_size(const uint32_t* mag_dev, const uint8_t* neg_dev,
+                                      const uint16_t* emax_dev, const uint8_t* planes_dev,
+                                      const uint8_t* raw_mask_dev, const uint32_t* raw_words_dev,
+                                      uint64_t n_blocks, int n_planes, int budget_bits,
+                                      int has_raw_flag, uint64_t* offsets_dev,
+                                      uint64_t* total_bits_host, whff_stream_t stream);
+/* Pass 2: emit into a zeroed device payload of >= ceil(total/8)+16 bytes.  */
+whff_status_t whff_encode_blocks_emit(const uint32_t* mag_dev, const uint8_t* neg_dev,
+                                      const uint16_t* emax_dev, const uint8_t* planes_dev,
+                                      const uint8_t* raw_mask_dev, const uint32_t* raw_words_dev,
+                                      uint64_t n_blocks, int n_planes, int budget_bits,
+                                      int has_raw_flag, const uint64_t* offsets_dev,
+                                      uint8_t* payload_dev, whff_stream_t stream);
+
+/* ------------------------------------------------------------------ */
+/* Codec: decode                                                        */
+/* ------------------------------------------------------------------ */
+
+/* Parity hook with exactly K:371-408 decode_blocks' outputs for blocks
+ * [first_block, first_block+count): mag u32[count*16], neg u8[count*16],
+ * emax u16[count], raw u8[count], raw_words u32[count*16],
+ * consumed u64[count] (all device).  planes_limit < 0: the stream's own
+ * (codec.py:301-303); n_planes is fixed at 27 (codec.py:28).              */
+whff_status_t whff_decode_blocks(whff_dstream_t s, uint64_t first_block, uint64_t count,
+                                 int planes_limit, uint32_t* mag_dev, uint8_t* neg_dev,
+                                 uint16_t* emax_dev, uint8_t* raw_dev, uint32_t* raw_words_dev,
+                                 uint64_t* consumed_dev, whff_stream_t stream);
+
+/* Reconstructed 4x4 blocks (codec.py:209-218 _reconstruct_blocks) for
+ * blocks [first_block, first_block+count): out_dev float32[count*16] raster
+ * order -- the device half of codec.py:317-332 decode_block.             */
+whff_status_t whff_decode_block_words(whff_dstream_t s, uint64_t first_block, uint64_t count,
+                                      float* out_dev, whff_stream_t stream);
+
+/* codec.py:296-314 decompress: float32 words, bit-exact, into out_dev
+ * (rows x cols, row pitch ld_out elements).  Non-finite decoded values are
+ * reported through status_dev (codec.py:312-313 -> CorruptStreamError).    */
+whff_status_t whff_decode(whff_dstream_t s, float* out_dev, uint64_t ld_out,
+                          uint64_t* status_dev, whff_stream_t stream);
+
+/* ------------------------------------------------------------------ */
+/* Fused decompress + GEMV (replaces codec.decompress followed by        */
+/* mpgemv.gemv, pipeline.py:146 + :199-205)                             */
+/* ------------------------------------------------------------------ */
+
+/* y[r - row_begin] = sum_j C[r, j] * v[j] for r in [row_begin, row_end),
+ * C the decoded stream.  v_dev has `cols` floats, y_dev row_end-row_begin.
+ * workspace: whff_decode_gemv_workspace_size bytes (device), or NULL if 0. */
+whff_status_t whff_decode_gemv_workspace_size(whff_dstream_t s, int eval, size_t* bytes);
+whff_status_t whff_decode_gemv(whff_dstream_t s, const float* v_dev, float* y_dev,
+                               int policy, int eval, uint64_t row_begin, uint64_t row_end,
+                               void* workspace_dev, size_t workspace_bytes,
+                               uint64_t* status_dev, whff_stream_t stream);
+
+/* Batched plan: n jobs (stream, vector, output, row range) executed by one
+ * persistent launch per call -- the per-light-step deformation products of
+ * pipeline.py:199-205 over many slit streams.  Creation builds the device
+ * job table (synchronous); launch is capture-safe (CUDA graphs).  All
+ * streams of a plan must share mode, index kind and raw flag.             */
+whff_status_t whff_gemv_plan_create(int n_jobs, const whff_dstream_t* streams,
+                                    const float* const* v_dev, float* const* y_dev,
+                                    const uint64_t* row_begin, const uint64_t* row_end,
+                                    int policy, int eval, whff_gemv_plan_t* out);
+whff_status_t whff_gemv_plan_launch(whff_gemv_plan_t plan, uint64_t* status_dev,
+                                    whff_stream_t stream);
+/* bytes the plan's launch reads (payload + index + vectors) and writes    */
+whff_status_t whff_gemv_plan_traffic(whff_gemv_plan_t plan, uint64_t* bytes_read,
+                                     uint64_t* bytes_written, uint64_t* n_blocks);
+whff_status_t whff_gemv_plan_destroy(whff_gemv_plan_t plan);
+
+/* ------------------------------------------------------------------ */
+/* Dense GEMV: the plugin's gemv_kernel (K:80-132)                       */
+/* ------------------------------------------------------------------ */
+
+whff_status_t whff_gemv_workspace_size(uint64_t rows, uint64_t cols, int policy, int shape,
+                                       int fanout, size_t* bytes);
+/* y[i] = sum_j A[i*lda + j] * v[j]; policy/shape/fanout as K:80-84.      */
+whff_status_t whff_gemv(const float* a_dev, uint64_t lda, uint64_t rows, uint64_t cols,
+                        const float* v_dev, float* y_dev, int policy, int shape, int fanout,
+                        void* workspace_dev, size_t workspace_bytes, whff_stream_t stream);
+/* binary64 ground truth (mpgemv.py:64-69 gemv_oracle): y64 = cumsum order */
+whff_status_t whff_gemv_oracle(const float* a_dev, uint64_t lda, uint64_t rows, uint64_t cols,
+                               const float* v_dev, double* y_dev, whff_stream_t stream);
+
+/* First non-finite element (mpgemv.py:42-51, codec.py:231, thermal.py:91-95):
+ * atomically lowers *status_dev to its flat index.                       */
+whff_status_t whff_find_nonfinite(const float* x_dev, uint64_t n, uint64_t* status_dev,
+                                  whff_stream_t stream);
+
+/* ------------------------------------------------------------------ */
+/* Thermal model (thermal.py:81-117)                                     */
+/* ------------------------------------------------------------------ */
+
+/* y = fp32(A64 x + diag(b) u): thermal.py:98-109 when b/u are given,
+ * thermal.py:112-117 (interpolation) when b_dev == u_dev == NULL.
+ * CSR with binary64 values accumulated in CSR order (scipy csr_matvec).  */
+whff_status_t whff_csr_matvec(const int64_t* indptr_dev, const int32_t* indices_dev,
+                              const double* data_dev, uint64_t n_rows, const float* x_dev,
+                              const float* b_dev, const float* u_dev, float* y_dev,
+                              whff_stream_t stream);
+/* u = fp32(fp32(dose) * footprint + dark) (thermal.py:81-88); footprint
+ * NULL = dark step (u = dark).                                           */
+whff_status_t whff_source_term(const float* footprint_dev, const float* dark_dev, float dose,
+                               uint64_t n, float* u_dev, whff_stream_t stream);
+
+#ifdef __cplusplus
+}
+#endif
+#endif /* WHFF_B200_H */

@@ -1,0 +1,1560 @@
+// whff_b200.cu -- sm_100a kernels and the C ABI of include/whff_b200.h.
+//
+// Hot path: k_decode_gemv, the fused WHFZ decode + mixed-precision GEMV
+// (reference: codec.decompress (codec.py:296-314, K:371-408) followed by
+// mpgemv.gemv(mixed, sequential) (mpgemv.py:54-61, K:24-47), as issued per
+// light step by pipeline._compute_deltas (pipeline.py:199-205)).  One warp
+// owns one 4-row block-row; lane l decodes block-columns l, l+32, ... so a
+// warp's 32 segments are contiguous in HBM (coalesced 16-byte loads at
+// FixedRate(8)); products accumulate per lane and reduce with a fixed xor
+// butterfly: deterministic, no atomics.
+//
+// Everything else here (decode-only, decode_blocks parity hook, GPU encoder,
+// dense GEMV policies, thermal CSR step) restates the reference operation
+// named at each kernel.
+#include <cuda_runtime.h>
+#include <cub/device/device_scan.cuh>
+
+#include <algorithm>
+#include <type_traits>
+#include <cstring>
+#include <string>
+#include <vector>
+
+#include "../../include/whff_b200.h"
+#include "whff_decode.cuh"
+#include "whff_encode.cuh"
+
+using namespace whff;
+
+// ---------------------------------------------------------------------------
+// error plumbing
+// ---------------------------------------------------------------------------
+namespace {
+thread_local std::string g_err;
+
+whff_status_t fail(whff_status_t s, const std::string& msg) {
+  g_err = msg;
+  return s;
+}
+whff_status_t cuda_fail(cudaError_t e, const char* what) {
+  g_err = std::string(what) + ": " + cudaGetErrorString(e);
+  return e == cudaErrorMemoryAllocation ? WHFF_ERR_NOMEM : WHFF_ERR_CUDA;
+}
+}  // namespace
+
+#define WCK(x)                                             \
+  do {                                                     \
+    cudaError_t e_ = (x);                                  \
+    if (e_ != cudaSuccess) return cuda_fail(e_, #x);       \
+  } while (0)
+#define WCK_LAUNCH(what)                                   \
+  do {                                                     \
+    cudaError_t e_ = cudaGetLastError();                   \
+    if (e_ != cudaSuccess) return cuda_fail(e_, what);     \
+  } while (0)
+
+// ---------------------------------------------------------------------------
+// device view of a stream
+// ---------------------------------------------------------------------------
+struct StreamView {
+  const uint32_t* words;     // payload as LE uint32 words (padded)
+  const uint64_t* base;      // COMPACT: start bit of block (br, 32g)
+  const uint16_t* lens;      // COMPACT/FULL: segment bits (clamped 65535)
+  const uint64_t* starts;    // FULL: start bit per block
+  uint64_t payload_bits;
+  uint64_t rows, cols, br, bc, gpr;
+  uint32_t seg_bits;         // IMPLICIT: 16 * bpv
+  int32_t kind;
+  int32_t planes_limit;
+  int32_t has_raw;
+};
+
+struct whff_dstream {
+  int device;
+  int mode;
+  double param;
+  uint64_t rows, cols, br, bc, nb, gpr;
+  uint64_t payload_bytes, payload_bits, total_bits = 0;
+  int planes_limit, has_raw, kind;
+  uint32_t seg_bits;
+  uint8_t* d_payload = nullptr;
+  size_t payload_alloc = 0;
+  uint64_t* d_base = nullptr;
+  uint16_t* d_lens = nullptr;
+  uint64_t* d_starts = nullptr;
+  size_t index_bytes = 0;
+
+  StreamView view() const {
+    StreamView v;
+    v.words = reinterpret_cast<const uint32_t*>(d_payload);
+    v.base = d_base;
+    v.lens = d_lens;
+    v.starts = d_starts;
+    v.payload_bits = payload_bits;
+    v.rows = rows;
+    v.cols = cols;
+    v.br = br;
+    v.bc = bc;
+    v.gpr = gpr;
+    v.seg_bits = seg_bits;
+    v.kind = kind;
+    v.planes_limit = planes_limit;
+    v.has_raw = has_raw;
+    return v;
+  }
+};
+
+__device__ __forceinline__ int clamp_len(uint64_t start, uint64_t seg, uint64_t payload_bits) {
+  if (start >= payload_bits) return 0;
+  uint64_t lim = start + seg;
+  if (lim > payload_bits) lim = payload_bits;
+  const uint64_t l = lim - start;
+  return l > 65535u ? 65535 : (int)l;
+}
+
+// start/len of one block, any index kind (COMPACT walks <= 31 lengths)
+__device__ void block_extent(const StreamView& s, uint64_t b, uint64_t& start, int& len) {
+  if (s.kind == WHFF_INDEX_IMPLICIT) {
+    start = b * (uint64_t)s.seg_bits;
+    len = clamp_len(start, s.seg_bits, s.payload_bits);
+  } else if (s.kind == WHFF_INDEX_FULL) {
+    start = s.starts[b];
+    len = clamp_len(start, s.lens[b], s.payload_bits);
+  } else {
+    const uint64_t brow = b / s.bc, bcol = b % s.bc;
+    const uint64_t g0 = bcol & ~31ull;
+    uint64_t st = s.base[brow * s.gpr + (bcol >> 5)];
+    for (uint64_t c = g0; c < bcol; ++c) st += s.lens[brow * s.bc + c];
+    start = st;
+    len = clamp_len(start, s.lens[b], s.payload_bits);
+  }
+}
+
+// ---------------------------------------------------------------------------
+// decode_blocks parity hook (K:371-408)
+// ---------------------------------------------------------------------------
+template <bool HAS_RAW>
+__global__ void __launch_bounds__(128) k_decode_blocks(StreamView s, uint64_t first, uint64_t count,
+                                                       int planes_limit, uint32_t* mag, uint8_t* neg,
+                                                       uint16_t* emax, uint8_t* raw,
+                                                       uint32_t* raw_words, uint64_t* consumed) {
+  const uint64_t i = blockIdx.x * (uint64_t)blockDim.x + threadIdx.x;
+  if (i >= count) return;
+  const uint64_t b = first + i;
+  uint64_t start;
+  int len;
+  block_extent(s, b, start, len);
+  BitWindow bw;
+  window_at(bw, s.words, start);
+  Decoded d;
+  decode_block<HAS_RAW, true>(bw, len, planes_limit, d);
+  emax[i] = (uint16_t)d.emax;
+  raw[i] = (uint8_t)d.raw;
+  consumed[i] = (uint64_t)d.consumed;
+#pragma unroll
+  for (int c = 0; c < 16; ++c) {
+    mag[16 * i + c] = d.raw ? 0u : d.mag[c];
+    raw_words[16 * i + c] = d.raw ? d.mag[c] : 0u;
+    neg[16 * i + c] = (uint8_t)((d.negm >> c) & 1u);
+  }
+}
+
+// ---------------------------------------------------------------------------
+// reconstructed blocks (codec.py:209-218), the device half of decode_block
+// ---------------------------------------------------------------------------
+template <bool HAS_RAW>
+__global__ void __launch_bounds__(128) k_decode_block_words(StreamView s, uint64_t first, uint64_t count,
+                                                            float* out) {
+  const uint64_t i = blockIdx.x * (uint64_t)blockDim.x + threadIdx.x;
+  if (i >= count) return;
+  uint64_t start;
+  int len;
+  block_extent(s, first + i, start, len);
+  BitWindow bw;
+  window_at(bw, s.words, start);
+  Decoded d;
+  decode_block<HAS_RAW, true>(bw, len, s.planes_limit, d);
+  float x[16];
+  reconstruct_words(d, x);
+#pragma unroll
+  for (int c = 0; c < 16; ++c) out[16 * i + c] = x[c];
+}
+
+// ---------------------------------------------------------------------------
+// decompress (codec.py:296-314): bit-exact words, non-finite -> status
+// ---------------------------------------------------------------------------
+template <bool HAS_RAW>
+__global__ void __launch_bounds__(128) k_decode_words(StreamView s, float* out, uint64_t ld,
+                                                      unsigned long long* status) {
+  const uint64_t b = blockIdx.x * (uint64_t)blockDim.x + threadIdx.x;
+  if (b >= s.br * s.bc) return;
+  uint64_t start;
+  int len;
+  block_extent(s, b, start, len);
+  BitWindow bw;
+  window_at(bw, s.words, start);
+  Decoded d;
+  decode_block<HAS_RAW, true>(bw, len, s.planes_limit, d);
+  float x[16];
+  reconstruct_words(d, x);
+  const uint64_t r0 = (b / s.bc) * 4, c0 = (b % s.bc) * 4;
+  unsigned long long bad = ~0ull;
+#pragma unroll
+  for (int i = 0; i < 4; ++i) {
+    const uint64_t r = r0 + i;
+    if (r >= s.rows) break;
+#pragma unroll
+    for (int j = 0; j < 4; ++j) {
+      const uint64_t c = c0 + j;
+      if (c < s.cols) {
+        out[r * ld + c] = x[4 * i + j];
+        if (!isfinite(x[4 * i + j])) {
+          const unsigned long long f = r * s.cols + c;
+          bad = f < bad ? f : bad;
+        }
+      }
+    }
+  }
+  if (bad != ~0ull) atomicMin(status, bad);
+}
+
+// ---------------------------------------------------------------------------
+// Fused decode + GEMV (the hot path)
+// ---------------------------------------------------------------------------
+struct GemvJob {
+  StreamView s;
+  const float* v;
+  const float4* U;     // coefficient domain: G^T v per block-column
+  float* y;
+  uint64_t row_begin, row_end;
+  uint64_t br0;        // first block-row of the job
+};
+
+struct JobTable {
+  const GemvJob* jobs;       // device table (plans) or nullptr
+  const uint64_t* prefix;    // first global warp of each job
+  int n;
+  uint64_t total_warps;
+  GemvJob single;            // used when jobs == nullptr
+};
+
+// G = real-valued inverse lift (codec.py:128-134 with >>1 -> /2, <<1 -> *2);
+// the decoded block is 2^(e-26) * G Q G^T up to lift rounding.
+__device__ __constant__ float c_G[4][4] = {{1.0f, 1.5f, -1.0f, -0.25f},
+                                          {1.0f, 0.5f, 1.0f, 1.25f},
+                                          {1.0f, -0.5f, 1.0f, -1.25f},
+                                          {1.0f, -1.5f, -1.0f, 0.25f}};
+
+// block-column vector slice, zero padded past cols
+__device__ __forceinline__ float4 load_v4(const float* v, uint64_t bcol, uint64_t cols, bool aligned) {
+  const uint64_t c0 = bcol * 4;
+  if (aligned && c0 + 3 < cols) return ldg(reinterpret_cast<const float4*>(v) + bcol);
+  float4 r;
+  r.x = c0 + 0 < cols ? ldg(v + c0 + 0) : 0.0f;
+  r.y = c0 + 1 < cols ? ldg(v + c0 + 1) : 0.0f;
+  r.z = c0 + 2 < cols ? ldg(v + c0 + 2) : 0.0f;
+  r.w = c0 + 3 < cols ? ldg(v + c0 + 3) : 0.0f;
+  return r;
+}
+
+// Accumulators for the three policies (mpgemv.py:1-7):
+//   mixed : binary32 product, binary64 sum     single: binary32 both
+//   double: binary64 product and sum
+struct Acc {
+  double d[4];
+  float f[4];
+  float probe;   // single policy: NaN iff a decoded value was non-finite
+};
+
+__device__ __forceinline__ void acc_exact(Acc& A, int policy, const float x[16], float4 v4,
+                                          uint32_t colmask) {
+  const float vv[4] = {v4.x, v4.y, v4.z, v4.w};
+#pragma unroll
+  for (int i = 0; i < 4; ++i) {
+#pragma unroll
+    for (int j = 0; j < 4; ++j) {
+      if (!((colmask >> j) & 1u)) continue;
+      const float xv = x[4 * i + j];
+      if (policy == WHFF_POLICY_MIXED) {
+        A.d[i] = __dadd_rn(A.d[i], (double)__fmul_rn(xv, vv[j]));
+      } else if (policy == WHFF_POLICY_SINGLE) {
+        A.f[i] = __fadd_rn(A.f[i], __fmul_rn(xv, vv[j]));
+        A.probe = __fmaf_rn(xv, 0.0f, A.probe);
+      } else {
+        A.d[i] = __dadd_rn(A.d[i], __dmul_rn((double)xv, (double)vv[j]));
+      }
+    }
+  }
+}
+
+// coefficient domain: w = Q u (Q at raster positions), acc += 2^k w
+__device__ __forceinline__ void acc_coeff(Acc& A, int policy, const Decoded& d, float4 u4, int k) {
+  const float u[4] = {u4.x, u4.y, u4.z, u4.w};
+  float w[4] = {0.0f, 0.0f, 0.0f, 0.0f};
+#pragma unroll
+  for (int c = 0; c < 16; ++c) {
+    const int pos = seq_pos(c);
+    float q = (float)d.mag[c];
+    q = ((d.negm >> c) & 1u) ? -q : q;
+    w[pos >> 2] = __fmaf_rn(q, u[pos & 3], w[pos >> 2]);
+  }
+  const float s = scale_f32(k);
+#pragma unroll
+  for (int a = 0; a < 4; ++a) {
+    const float t = __fmul_rn(w[a], s);
+    if (policy == WHFF_POLICY_SINGLE) A.f[a] = __fadd_rn(A.f[a], t);
+    else A.d[a] = __dadd_rn(A.d[a], (double)t);
+  }
+}
+
+template <int VAR>
+struct VarTraits;
+// 0: FixedRate(8) implicit index, one 16-byte load per block, no refill
+template <> struct VarTraits<0> { static constexpr bool kRefill = false, kRaw = false, kIndexed = false; };
+// 1: any implicit fixed rate
+template <> struct VarTraits<1> { static constexpr bool kRefill = true, kRaw = false, kIndexed = false; };
+// 2: indexed (compact/full), no raw flag (fixed precision / odd rate offsets)
+template <> struct VarTraits<2> { static constexpr bool kRefill = true, kRaw = false, kIndexed = true; };
+// 3: indexed with raw flag (fixed accuracy)
+template <> struct VarTraits<3> { static constexpr bool kRefill = true, kRaw = true, kIndexed = true; };
+
+template <int VAR, int EVAL>
+__global__ void __launch_bounds__(256) k_decode_gemv(JobTable T, int policy,
+                                                     unsigned long long* status) {
+  using TR = VarTraits<VAR>;
+  const uint64_t gw = (blockIdx.x * (uint64_t)blockDim.x + threadIdx.x) >> 5;
+  if (gw >= T.total_warps) return;
+  const int lane = threadIdx.x & 31;
+
+  uint64_t first_warp = 0;
+  int jidx = -1;
+  if (T.jobs != nullptr) {
+    int lo = 0, hi = T.n - 1;
+    while (lo < hi) {
+      const int mid = (lo + hi + 1) >> 1;
+      if (T.prefix[mid] <= gw) lo = mid; else hi = mid - 1;
+    }
+    jidx = lo;
+    first_warp = T.prefix[lo];
+  }
+  const StreamView s = jidx < 0 ? T.single.s : T.jobs[jidx].s;
+  const float* __restrict__ v = jidx < 0 ? T.single.v : T.jobs[jidx].v;
+  const float4* __restrict__ U = jidx < 0 ? T.single.U : T.jobs[jidx].U;
+  float* __restrict__ yout = jidx < 0 ? T.single.y : T.jobs[jidx].y;
+  const uint64_t row_begin = jidx < 0 ? T.single.row_begin : T.jobs[jidx].row_begin;
+  const uint64_t row_end = jidx < 0 ? T.single.row_end : T.jobs[jidx].row_end;
+  const uint64_t br0 = jidx < 0 ? T.single.br0 : T.jobs[jidx].br0;
+  const uint64_t brow = br0 + (gw - first_warp);
+  const uint64_t bc = s.bc;
+  const bool v_aligned = ((reinterpret_cast<uintptr_t>(v) & 15u) == 0);
+  const uint32_t last_colmask = (s.cols & 3) ? ((1u << (s.cols & 3)) - 1u) : 0xFu;
+  const int pl = s.planes_limit;
+
+  Acc A;
+#pragma unroll
+  for (int i = 0; i < 4; ++i) { A.d[i] = 0.0; A.f[i] = 0.0f; }
+  A.probe = 0.0f;
+  double accR[4] = {0.0, 0.0, 0.0, 0.0};   // coefficient domain: exact raw-block part
+  float accRf[4] = {0.0f, 0.0f, 0.0f, 0.0f};
+
+  const uint64_t row_block0 = brow * bc;
+  const uint4* __restrict__ seg128 = reinterpret_cast<const uint4*>(s.words);
+  uint4 nxt = make_uint4(0, 0, 0, 0);
+  if (VAR == 0 && (uint64_t)lane < bc) nxt = ldg(seg128 + row_block0 + lane);
+
+  for (uint64_t g = 0; g < s.gpr; ++g) {
+    const uint64_t bcol = g * 32 + lane;
+    const bool active = bcol < bc;
+    const uint64_t b = row_block0 + bcol;
+    BitWindow bw;
+    int len = 0;
+    if (VAR == 0) {
+      const uint4 q = nxt;
+      if (bcol + 32 < bc) nxt = ldg(seg128 + b + 32);   // prefetch next group
+      bw.w0 = bswap32(q.x); bw.w1 = bswap32(q.y); bw.w2 = bswap32(q.z); bw.w3 = bswap32(q.w);
+      bw.off = 0;
+      bw.src = nullptr;
+      len = clamp_len(b * 128ull, 128ull, s.payload_bits);
+    } else if (!TR::kIndexed) {
+      const uint64_t start = b * (uint64_t)s.seg_bits;
+      len = active ? clamp_len(start, s.seg_bits, s.payload_bits) : 0;
+      if (active) window_at(bw, s.words, start);
+    } else {
+      uint64_t start = 0;
+      if (s.kind == WHFF_INDEX_COMPACT) {
+        const uint32_t l = active ? (uint32_t)s.lens[b] : 0u;
+        uint32_t incl = l;
+#pragma unroll
+        for (int o = 1; o < 32; o <<= 1) {
+          const uint32_t t = __shfl_up_sync(0xFFFFFFFFu, incl, o);
+          if (lane >= o) incl += t;
+        }
+        start = s.base[brow * s.gpr + g] + (incl - l);
+        len = active ? clamp_len(start, l, s.payload_bits) : 0;
+      } else if (active) {
+        start = s.starts[b];
+        len = clamp_len(start, s.lens[b], s.payload_bits);
+      }
+      if (active) window_at(bw, s.words, start);
+    }
+    if (!active) continue;
+
+    Decoded d;
+    decode_block<TR::kRaw, TR::kRefill>(bw, len, pl, d);
+    const uint32_t colmask = (bcol + 1 == bc) ? last_colmask : 0xFu;
+
+    if (EVAL == WHFF_EVAL_EXACT) {
+      const float4 v4 = load_v4(v, bcol, s.cols, v_aligned);
+      float x[16];
+      reconstruct_words(d, x);
+      acc_exact(A, policy, x, v4, colmask);
+    } else {
+      if (d.raw || d.emax == 0) {
+        if (d.raw) {
+          const float4 v4 = load_v4(v, bcol, s.cols, v_aligned);
+          float x[16];
+          reconstruct_words(d, x);
+          Acc R;
+#pragma unroll
+          for (int i = 0; i < 4; ++i) { R.d[i] = accR[i]; R.f[i] = accRf[i]; }
+          R.probe = A.probe;
+          acc_exact(R, policy, x, v4, colmask);
+#pragma unroll
+          for (int i = 0; i < 4; ++i) { accR[i] = R.d[i]; accRf[i] = R.f[i]; }
+          A.probe = R.probe;
+        }
+      } else {
+        const int k = (int)d.emax - kEmaxBias - kQuantBits;
+        if (k >= -126 && k <= 100) {
+          acc_coeff(A, policy, d, ldg(U + bcol), k);
+        } else {  // out of the normal fp32 scale range: exact spatial path
+          const float4 v4 = load_v4(v, bcol, s.cols, v_aligned);
+          float x[16];
+          reconstruct_words(d, x);
+          Acc R;
+#pragma unroll
+          for (int i = 0; i < 4; ++i) { R.d[i] = accR[i]; R.f[i] = accRf[i]; }
+          R.probe = A.probe;
+          acc_exact(R, policy, x, v4, colmask);
+#pragma unroll
+          for (int i = 0; i < 4; ++i) { accR[i] = R.d[i]; accRf[i] = R.f[i]; }
+          A.probe = R.probe;
+        }
+      }
+    }
+  }
+
+  // fixed xor butterfly over the warp (deterministic)
+#pragma unroll
+  for (int o = 16; o > 0; o >>= 1) {
+#pragma unroll
+    for (int i = 0; i < 4; ++i) {
+      A.d[i] = __dadd_rn(A.d[i], __shfl_xor_sync(0xFFFFFFFFu, A.d[i], o));
+      A.f[i] = __fadd_rn(A.f[i], __shfl_xor_sync(0xFFFFFFFFu, A.f[i], o));
+      if (EVAL == WHFF_EVAL_COEFF) {
+        accR[i] = __dadd_rn(accR[i], __shfl_xor_sync(0xFFFFFFFFu, accR[i], o));
+        accRf[i] = __fadd_rn(accRf[i], __shfl_xor_sync(0xFFFFFFFFu, accRf[i], o));
+      }
+    }
+    A.probe = __fadd_rn(A.probe, __shfl_xor_sync(0xFFFFFFFFu, A.probe, o));
+  }
+  if (lane < 4) {
+    const int i = lane;
+    const uint64_t r = brow * 4 + i;
+    if (r >= row_begin && r < row_end && r < s.rows) {
+      float out;
+      bool bad;
+      if (EVAL == WHFF_EVAL_EXACT) {
+        if (policy == WHFF_POLICY_SINGLE) {
+          out = A.f[i];
+          bad = !isfinite(A.probe);
+        } else {
+          out = __double2float_rn(A.d[i]);
+          bad = !isfinite(A.d[i]);
+        }
+      } else {
+        if (policy == WHFF_POLICY_SINGLE) {
+          float t = accRf[i];
+#pragma unroll
+          for (int a = 0; a < 4; ++a) t = __fmaf_rn(c_G[i][a], A.f[a], t);
+          out = t;
+          bad = !isfinite(A.probe);
+        } else {
+          double t = accR[i];
+#pragma unroll
+          for (int a = 0; a < 4; ++a) t = __fma_rn((double)c_G[i][a], A.d[a], t);
+          out = __double2float_rn(t);
+          bad = !isfinite(t);
+        }
+      }
+      yout[r - row_begin] = out;
+      if (bad) atomicMin(status, (unsigned long long)r);
+    }
+  }
+}
+
+// u_b = G^T v_b per block-column (coefficient-domain prologue)
+__global__ void k_coeff_prep(const float* v, uint64_t cols, uint64_t bc, float4* U) {
+  const uint64_t b = blockIdx.x * (uint64_t)blockDim.x + threadIdx.x;
+  if (b >= bc) return;
+  const float4 x = load_v4(v, b, cols, false);
+  const float xv[4] = {x.x, x.y, x.z, x.w};
+  float u[4];
+#pragma unroll
+  for (int k = 0; k < 4; ++k) {
+    double t = 0.0;
+#pragma unroll
+    for (int j = 0; j < 4; ++j) t += (double)c_G[j][k] * (double)xv[j];
+    u[k] = (float)t;
+  }
+  U[b] = make_float4(u[0], u[1], u[2], u[3]);
+}
+
+// ---------------------------------------------------------------------------
+// Dense GEMV policies (K:24-132)
+// ---------------------------------------------------------------------------
+// strict left-to-right per row (K:24-47); one thread per row.
+template <int POL, bool F64OUT>
+__global__ void k_gemv_seq(const float* A, uint64_t lda, uint64_t rows, uint64_t cols,
+                           const float* v, float* y, double* y64) {
+  const uint64_t i = blockIdx.x * (uint64_t)blockDim.x + threadIdx.x;
+  if (i >= rows) return;
+  const float* row = A + i * lda;
+  if (POL == WHFF_POLICY_SINGLE) {
+    float acc = 0.0f;
+    for (uint64_t j = 0; j < cols; ++j) acc = __fadd_rn(acc, __fmul_rn(row[j], ldg(v + j)));
+    y[i] = acc;
+  } else {
+    double acc = 0.0;
+    for (uint64_t j = 0; j < cols; ++j) {
+      const double p = POL == WHFF_POLICY_DOUBLE ? __dmul_rn((double)row[j], (double)ldg(v + j))
+                                                 : (double)__fmul_rn(row[j], ldg(v + j));
+      acc = __dadd_rn(acc, p);
+    }
+    if (F64OUT) y64[i] = acc;
+    else y[i] = __double2float_rn(acc);
+  }
+}
+
+// fixed-fanout tree (K:50-77): leaf level from products, groups summed
+// left to right, tail padded with zeros.  out is rows x ng.
+template <int POL, typename T>
+__global__ void k_gemv_tree_leaf(const float* A, uint64_t lda, uint64_t rows, uint64_t cols,
+                                 const float* v, int fanout, T* out, uint64_t ng) {
+  const uint64_t t = blockIdx.x * (uint64_t)blockDim.x + threadIdx.x;
+  if (t >= rows * ng) return;
+  const uint64_t i = t / ng, g = t % ng;
+  const float* row = A + i * lda;
+  auto prod = [&](uint64_t j) -> T {
+    if (POL == WHFF_POLICY_DOUBLE) return (T)__dmul_rn((double)row[j], (double)ldg(v + j));
+    return (T)__fmul_rn(row[j], ldg(v + j));
+  };
+  const uint64_t j0 = g * (uint64_t)fanout;
+  T acc = prod(j0);
+  for (int k = 1; k < fanout; ++k) {
+    const uint64_t j = j0 + k;
+    const T term = j < cols ? prod(j) : (T)0;
+    acc = acc + term;
+  }
+  out[i * ng + g] = acc;
+}
+
+template <typename T>
+__global__ void k_gemv_tree_level(const T* in, uint64_t rows, uint64_t w, int fanout, T* out,
+                                  uint64_t ng) {
+  const uint64_t t = blockIdx.x * (uint64_t)blockDim.x + threadIdx.x;
+  if (t >= rows * ng) return;
+  const uint64_t i = t / ng, g = t % ng;
+  const T* r = in + i * w;
+  const uint64_t j0 = g * (uint64_t)fanout;
+  T acc = r[j0];
+  for (int k = 1; k < fanout; ++k) {
+    const uint64_t j = j0 + k;
+    acc = acc + (j < w ? r[j] : (T)0);
+  }
+  out[i * ng + g] = acc;
+}
+
+template <typename T>
+__global__ void k_tree_store(const T* in, uint64_t rows, float* y) {
+  const uint64_t i = blockIdx.x * (uint64_t)blockDim.x + threadIdx.x;
+  if (i < rows) y[i] = (float)in[i];
+}
+
+// B200 blocked order: warp per (row, segment of seg_cols columns), float4
+// loads, per-lane accumulation, xor butterfly; partials summed in segment
+// order by k_blocked_finish.  Deterministic for a given shape.
+template <int POL>
+__global__ void __launch_bounds__(256) k_gemv_blocked(const float* A, uint64_t lda, uint64_t rows,
+                                                      uint64_t cols, const float* v, uint64_t nseg,
+                                                      uint64_t seg_cols, bool vec4, double* part) {
+  const uint64_t gw = (blockIdx.x * (uint64_t)blockDim.x + threadIdx.x) >> 5;
+  if (gw >= rows * nseg) return;
+  const int lane = threadIdx.x & 31;
+  const uint64_t i = gw / nseg, sg = gw % nseg;
+  const float* row = A + i * lda;
+  const uint64_t c0 = sg * seg_cols;
+  const uint64_t c1 = min(cols, c0 + seg_cols);
+  double accd = 0.0;
+  float accf = 0.0f;
+  auto add = [&](float a, float b) {
+    if (POL == WHFF_POLICY_SINGLE) accf = __fadd_rn(accf, __fmul_rn(a, b));
+    else if (POL == WHFF_POLICY_MIXED) accd = __dadd_rn(accd, (double)__fmul_rn(a, b));
+    else accd = __dadd_rn(accd, __dmul_rn((double)a, (double)b));
+  };
+  if (vec4) {
+    const float4* r4 = reinterpret_cast<const float4*>(row);
+    const float4* v4 = reinterpret_cast<const float4*>(v);
+    for (uint64_t q = c0 / 4 + lane; q < c1 / 4; q += 32) {
+      const float4 a = ldg(r4 + q), b = ldg(v4 + q);
+      add(a.x, b.x); add(a.y, b.y); add(a.z, b.z); add(a.w, b.w);
+    }
+    for (uint64_t j = (c1 / 4) * 4 + lane; j < c1; j += 32) add(row[j], ldg(v + j));
+  } else {
+    for (uint64_t j = c0 + lane; j < c1; j += 32) add(row[j], ldg(v + j));
+  }
+#pragma unroll
+  for (int o = 16; o > 0; o >>= 1) {
+    accd = __dadd_rn(accd, __shfl_xor_sync(0xFFFFFFFFu, accd, o));
+    accf = __fadd_rn(accf, __shfl_xor_sync(0xFFFFFFFFu, accf, o));
+  }
+  if (lane == 0) part[gw] = POL == WHFF_POLICY_SINGLE ? (double)accf : accd;
+}
+
+template <int POL>
+__global__ void k_blocked_finish(const double* part, uint64_t rows, uint64_t nseg, float* y) {
+  const uint64_t i = blockIdx.x * (uint64_t)blockDim.x + threadIdx.x;
+  if (i >= rows) return;
+  if (POL == WHFF_POLICY_SINGLE) {
+    float acc = 0.0f;
+    for (uint64_t s = 0; s < nseg; ++s) acc = __fadd_rn(acc, (float)part[i * nseg + s]);
+    y[i] = acc;
+  } else {
+    double acc = 0.0;
+    for (uint64_t s = 0; s < nseg; ++s) acc = __dadd_rn(acc, part[i * nseg + s]);
+    y[i] = __double2float_rn(acc);
+  }
+}
+
+__global__ void k_find_nonfinite(const float* x, uint64_t n, unsigned long long* status) {
+  const uint64_t stride = (uint64_t)gridDim.x * blockDim.x;
+  unsigned long long bad = ~0ull;
+  for (uint64_t i = blockIdx.x * (uint64_t)blockDim.x + threadIdx.x; i < n; i += stride) {
+    if (!isfinite(ldg(x + i))) { bad = i; break; }
+  }
+  if (bad != ~0ull) atomicMin(status, bad);
+}
+
+// ---------------------------------------------------------------------------
+// Thermal (thermal.py:81-117): CSR binary64, CSR order, binary32 store
+// ---------------------------------------------------------------------------
+__global__ void k_csr_matvec(const int64_t* indptr, const int32_t* indices, const double* data,
+                             uint64_t n, const float* x, const float* bdiag, const float* u,
+                             float* y) {
+  const uint64_t i = blockIdx.x * (uint64_t)blockDim.x + threadIdx.x;
+  if (i >= n) return;
+  double acc = 0.0;
+  const int64_t e = indptr[i + 1];
+  for (int64_t jj = indptr[i]; jj < e; ++jj)
+    acc = __dadd_rn(acc, __dmul_rn(ldg(data + jj), (double)ldg(x + ldg(indices + jj))));
+  if (bdiag != nullptr) acc = __dadd_rn(acc, __dmul_rn((double)bdiag[i], (double)u[i]));
+  y[i] = __double2float_rn(acc);
+}
+
+__global__ void k_source_term(const float* fp, const float* dark, float dose, uint64_t n, float* u) {
+  const uint64_t i = blockIdx.x * (uint64_t)blockDim.x + threadIdx.x;
+  if (i >= n) return;
+  u[i] = fp ? __fadd_rn(__fmul_rn(dose, fp[i]), dark[i]) : dark[i];
+}
+
+// ---------------------------------------------------------------------------
+// GPU encoder (codec.py:225-293, K:139-283)
+// ---------------------------------------------------------------------------
+__global__ void k_encode_len(const float* a, uint64_t lda, uint64_t rows, uint64_t cols, uint64_t nb,
+                             uint64_t bc, int mode, double param, uint64_t* lens, int* overflow) {
+  const uint64_t b = blockIdx.x * (uint64_t)blockDim.x + threadIdx.x;
+  if (b >= nb) return;
+  BlockPlan pl;
+  plan_block(a, (int64_t)lda, (int64_t)rows, (int64_t)cols, (int64_t)b, (int64_t)bc, mode, param, pl);
+  if (!pl.ok) atomicOr(overflow, 1);
+  const int budget = mode == WHFF_MODE_RATE ? (int)param * 16 : 0;
+  CountSink cs;
+  int n = encode_one(pl.mag, pl.negm, pl.code, pl.planes, pl.raw, pl.raw_words, budget,
+                     mode == WHFF_MODE_ACCURACY, cs);
+  if (budget) n = budget;
+  lens[b] = (uint64_t)n;
+}
+
+__global__ void k_encode_emit(const float* a, uint64_t lda, uint64_t rows, uint64_t cols, uint64_t nb,
+                              uint64_t bc, int mode, double param, const uint64_t* offsets,
+                              uint32_t* words) {
+  const uint64_t b = blockIdx.x * (uint64_t)blockDim.x + threadIdx.x;
+  if (b >= nb) return;
+  BlockPlan pl;
+  plan_block(a, (int64_t)lda, (int64_t)rows, (int64_t)cols, (int64_t)b, (int64_t)bc, mode, param, pl);
+  const int budget = mode == WHFF_MODE_RATE ? (int)param * 16 : 0;
+  WordSink ws{words, offsets[b], 0u, 0};
+  encode_one(pl.mag, pl.negm, pl.code, pl.planes, pl.raw, pl.raw_words, budget,
+             mode == WHFF_MODE_ACCURACY, ws);
+  ws.finish();
+}
+
+struct EncArrays {
+  const uint32_t* mag;
+  const uint8_t* neg;
+  const uint16_t* emax;
+  const uint8_t* planes;
+  const uint8_t* raw_mask;
+  const uint32_t* raw_words;
+};
+
+__device__ void load_enc(const EncArrays& E, uint64_t b, int has_raw, uint32_t mag[16],
+                         uint32_t& negm, uint32_t& code, int& planes, bool& raw, uint32_t rw[16]) {
+  negm = 0;
+#pragma unroll
+  for (int c = 0; c < 16; ++c) {
+    mag[c] = E.mag[16 * b + c];
+    if (E.neg[16 * b + c]) negm |= 1u << c;
+    rw[c] = E.raw_words[16 * b + c];
+  }
+  code = E.emax[b];
+  planes = E.planes[b];
+  raw = has_raw && E.raw_mask[b];
+}
+
+__global__ void k_encblocks_len(EncArrays E, uint64_t nb, int budget, int has_raw, uint64_t* lens) {
+  const uint64_t b = blockIdx.x * (uint64_t)blockDim.x + threadIdx.x;
+  if (b >= nb) return;
+  uint32_t mag[16], rw[16], negm, code;
+  int planes;
+  bool raw;
+  load_enc(E, b, has_raw, mag, negm, code, planes, raw, rw);
+  CountSink cs;
+  int n = encode_one(mag, negm, code, planes, raw, rw, budget, has_raw != 0, cs);
+  if (budget) n = budget;
+  lens[b] = (uint64_t)n;
+}
+
+__global__ void k_encblocks_emit(EncArrays E, uint64_t nb, int budget, int has_raw,
+                                 const uint64_t* offsets, uint32_t* words) {
+  const uint64_t b = blockIdx.x * (uint64_t)blockDim.x + threadIdx.x;
+  if (b >= nb) return;
+  uint32_t mag[16], rw[16], negm, code;
+  int planes;
+  bool raw;
+  load_enc(E, b, has_raw, mag, negm, code, planes, raw, rw);
+  WordSink ws{words, offsets[b], 0u, 0};
+  encode_one(mag, negm, code, planes, raw, rw, budget, has_raw != 0, ws);
+  ws.finish();
+}
+
+// compact index from u64 offsets (device-encoded streams)
+__global__ void k_build_compact(const uint64_t* offsets, uint64_t nb, uint64_t bc, uint64_t gpr,
+                                uint64_t payload_bits, uint16_t* lens, uint64_t* base) {
+  const uint64_t b = blockIdx.x * (uint64_t)blockDim.x + threadIdx.x;
+  if (b >= nb) return;
+  const uint64_t s = offsets[b];
+  const uint64_t e = b + 1 < nb ? offsets[b + 1] : payload_bits;
+  const uint64_t l = e > s ? e - s : 0;
+  lens[b] = (uint16_t)(l > 65535 ? 65535 : l);
+  const uint64_t brow = b / bc, bcol = b % bc;
+  if ((bcol & 31) == 0) base[brow * gpr + (bcol >> 5)] = s;
+}
+
+// ---------------------------------------------------------------------------
+// host helpers
+// ---------------------------------------------------------------------------
+namespace {
+
+inline unsigned grid_for(uint64_t n, unsigned t) { return (unsigned)((n + t - 1) / t); }
+
+struct DeviceGuard {
+  int prev = -1;
+  explicit DeviceGuard(int dev) {
+    cudaGetDevice(&prev);
+    if (dev >= 0 && dev != prev) cudaSetDevice(dev);
+  }
+  ~DeviceGuard() {
+    if (prev >= 0) cudaSetDevice(prev);
+  }
+};
+
+int planes_limit_for(int mode, double param) {
+  if (mode == WHFF_MODE_PRECISION) {
+    const int p = (int)param;
+    return p < kNPlanes ? p : kNPlanes;
+  }
+  return kNPlanes;
+}
+
+whff_status_t check_mode(int mode, double param) {
+  if (mode == WHFF_MODE_RATE) {
+    if (!(param >= 1 && param <= 32 && param == (double)(int)param))
+      return fail(WHFF_ERR_ARGUMENT, "fixed-rate bits per value must be in 1..32");
+  } else if (mode == WHFF_MODE_PRECISION) {
+    if (!(param >= 1 && param <= 32 && param == (double)(int)param))
+      return fail(WHFF_ERR_ARGUMENT, "fixed-precision planes must be in 1..32");
+  } else if (mode == WHFF_MODE_ACCURACY) {
+    if (!(param >= 0.0)) return fail(WHFF_ERR_ARGUMENT, "tolerance must be nonnegative");
+  } else {
+    return fail(WHFF_ERR_ARGUMENT, "unknown codec mode");
+  }
+  return WHFF_OK;
+}
+
+whff_status_t alloc_payload(whff_dstream* s, uint64_t bytes) {
+  s->payload_alloc = ((bytes + 15) / 16) * 16 + 64;  // >= 32 readable pad bytes
+  WCK(cudaMalloc(&s->d_payload, s->payload_alloc));
+  WCK(cudaMemset(s->d_payload, 0, s->payload_alloc));
+  return WHFF_OK;
+}
+
+void free_stream(whff_dstream* s) {
+  if (!s) return;
+  DeviceGuard g(s->device);
+  cudaFree(s->d_payload);
+  cudaFree(s->d_base);
+  cudaFree(s->d_lens);
+  cudaFree(s->d_starts);
+  delete s;
+}
+
+}  // namespace
+
+// ---------------------------------------------------------------------------
+// C ABI
+// ---------------------------------------------------------------------------
+extern "C" {
+
+int whff_abi_version(void) { return WHFF_ABI_VERSION; }
+
+const char* whff_status_string(whff_status_t s) {
+  switch (s) {
+    case WHFF_OK: return "ok";
+    case WHFF_ERR_DIMENSION: return "dimension error";
+    case WHFF_ERR_NONFINITE: return "non-finite value";
+    case WHFF_ERR_CORRUPT: return "corrupt stream";
+    case WHFF_ERR_ARGUMENT: return "invalid argument";
+    case WHFF_ERR_OVERFLOW: return "internal error: transform coefficient overflow";
+    case WHFF_ERR_NOMEM: return "out of memory";
+    case WHFF_ERR_CUDA: return "cuda error";
+  }
+  return "unknown";
+}
+
+const char* whff_last_error(void) { return g_err.c_str(); }
+
+whff_status_t whff_dstream_create(int device, int mode, double param, uint64_t rows, uint64_t cols,
+                                  const uint8_t* payload, uint64_t payload_bytes,
+                                  const uint64_t* index, uint64_t nb, whff_dstream_t* out) {
+  if (!out) return fail(WHFF_ERR_ARGUMENT, "null output handle");
+  *out = nullptr;
+  whff_status_t st = check_mode(mode, param);
+  if (st != WHFF_OK) return st;
+  if (rows < 1 || cols < 1) return fail(WHFF_ERR_DIMENSION, "stream dimensions must be positive");
+  const uint64_t br = (rows + 3) / 4, bc = (cols + 3) / 4;
+  // codec.py:347-356 _validate_stream
+  if (nb != br * bc) return fail(WHFF_ERR_CORRUPT, "block index length does not match dimensions");
+  if (payload_bytes > 0 && !payload) return fail(WHFF_ERR_ARGUMENT, "null payload");
+  if (!index) return fail(WHFF_ERR_ARGUMENT, "null block index");
+  const uint64_t pbits = payload_bytes * 8;
+  uint64_t mx = 0;
+  for (uint64_t b = 0; b < nb; ++b) mx = index[b] > mx ? index[b] : mx;
+  if (mx >= std::max<uint64_t>(pbits, 1))
+    return fail(WHFF_ERR_CORRUPT, "block index offsets point past the payload");
+  // codec.py:335-344 _segment_lengths (variable modes)
+  if (mode != WHFF_MODE_RATE) {
+    for (uint64_t b = 0; b + 1 < nb; ++b)
+      if (index[b + 1] < index[b])
+        return fail(WHFF_ERR_CORRUPT, "block index offsets are not nondecreasing");
+  }
+  DeviceGuard g(device);
+  whff_dstream* s = new whff_dstream();
+  s->device = device;
+  s->mode = mode;
+  s->param = param;
+  s->rows = rows;
+  s->cols = cols;
+  s->br = br;
+  s->bc = bc;
+  s->nb = nb;
+  s->gpr = (bc + 31) / 32;
+  s->payload_bytes = payload_bytes;
+  s->payload_bits = pbits;
+  s->planes_limit = planes_limit_for(mode, param);
+  s->has_raw = mode == WHFF_MODE_ACCURACY;
+  s->seg_bits = mode == WHFF_MODE_RATE ? (uint32_t)param * 16u : 0u;
+  st = alloc_payload(s, payload_bytes);
+  if (st != WHFF_OK) { free_stream(s); return st; }
+  if (payload_bytes) {
+    cudaError_t e = cudaMemcpy(s->d_payload, payload, payload_bytes, cudaMemcpyHostToDevice);
+    if (e != cudaSuccess) { free_stream(s); return cuda_fail(e, "upload payload"); }
+  }
+  // choose the index layout
+  bool implicit = mode == WHFF_MODE_RATE;
+  for (uint64_t b = 0; implicit && b < nb; ++b) implicit = index[b] == b * s->seg_bits;
+  std::vector<uint16_t> lens;
+  if (implicit) {
+    s->kind = WHFF_INDEX_IMPLICIT;
+  } else {
+    lens.resize(nb);
+    bool compact = mode != WHFF_MODE_RATE;
+    for (uint64_t b = 0; b < nb; ++b) {
+      uint64_t l;
+      if (mode == WHFF_MODE_RATE) {
+        l = s->seg_bits;
+      } else {
+        const uint64_t e = b + 1 < nb ? index[b + 1] : pbits;
+        l = e - index[b];
+        if (b + 1 < nb && l > 65535) compact = false;
+      }
+      lens[b] = (uint16_t)(l > 65535 ? 65535 : l);
+    }
+    s->kind = compact ? WHFF_INDEX_COMPACT : WHFF_INDEX_FULL;
+    cudaError_t e = cudaMalloc(&s->d_lens, nb * sizeof(uint16_t));
+    if (e == cudaSuccess) e = cudaMemcpy(s->d_lens, lens.data(), nb * 2, cudaMemcpyHostToDevice);
+    if (e == cudaSuccess) {
+      if (compact) {
+        std::vector<uint64_t> base(br * s->gpr);
+        for (uint64_t r = 0; r < br; ++r)
+          for (uint64_t gg = 0; gg < s->gpr; ++gg) base[r * s->gpr + gg] = index[r * bc + gg * 32];
+        e = cudaMalloc(&s->d_base, base.size() * 8);
+        if (e == cudaSuccess) e = cudaMemcpy(s->d_base, base.data(), base.size() * 8, cudaMemcpyHostToDevice);
+        s->index_bytes = nb * 2 + base.size() * 8;
+      } else {
+        e = cudaMalloc(&s->d_starts, nb * 8);
+        if (e == cudaSuccess) e = cudaMemcpy(s->d_starts, index, nb * 8, cudaMemcpyHostToDevice);
+        s->index_bytes = nb * 10;
+      }
+    }
+    if (e != cudaSuccess) { free_stream(s); return cuda_fail(e, "upload index"); }
+  }
+  *out = s;
+  return WHFF_OK;
+}
+
+whff_status_t whff_dstream_create_segments(int device, const uint8_t* payload, uint64_t payload_bytes,
+                                           const uint64_t* offsets, const uint64_t* seglens, uint64_t nb,
+                                           int planes_limit, int has_raw, whff_dstream_t* out) {
+  if (!out) return fail(WHFF_ERR_ARGUMENT, "null output handle");
+  *out = nullptr;
+  if (nb == 0) return fail(WHFF_ERR_DIMENSION, "empty segment table");
+  if ((payload_bytes && !payload) || !offsets || !seglens) return fail(WHFF_ERR_ARGUMENT, "null argument");
+  DeviceGuard g(device);
+  whff_dstream* s = new whff_dstream();
+  s->device = device;
+  s->mode = has_raw ? WHFF_MODE_ACCURACY : WHFF_MODE_PRECISION;
+  s->param = planes_limit;
+  s->rows = 4;
+  s->cols = 4 * nb;
+  s->br = 1;
+  s->bc = nb;
+  s->nb = nb;
+  s->gpr = (nb + 31) / 32;
+  s->payload_bytes = payload_bytes;
+  s->payload_bits = payload_bytes * 8;
+  s->planes_limit = planes_limit < 0 ? kNPlanes : std::min(planes_limit, kNPlanes);
+  s->has_raw = has_raw != 0;
+  s->seg_bits = 0;
+  s->kind = WHFF_INDEX_FULL;
+  whff_status_t st = alloc_payload(s, payload_bytes);
+  if (st != WHFF_OK) { free_stream(s); return st; }
+  std::vector<uint16_t> lens(nb);
+  for (uint64_t b = 0; b < nb; ++b) lens[b] = (uint16_t)std::min<uint64_t>(seglens[b], 65535);
+  cudaError_t e = payload_bytes ? cudaMemcpy(s->d_payload, payload, payload_bytes, cudaMemcpyHostToDevice)
+                                : cudaSuccess;
+  if (e == cudaSuccess) e = cudaMalloc(&s->d_lens, nb * 2);
+  if (e == cudaSuccess) e = cudaMemcpy(s->d_lens, lens.data(), nb * 2, cudaMemcpyHostToDevice);
+  if (e == cudaSuccess) e = cudaMalloc(&s->d_starts, nb * 8);
+  if (e == cudaSuccess) e = cudaMemcpy(s->d_starts, offsets, nb * 8, cudaMemcpyHostToDevice);
+  if (e != cudaSuccess) { free_stream(s); return cuda_fail(e, "segment stream upload"); }
+  s->index_bytes = nb * 10;
+  *out = s;
+  return WHFF_OK;
+}
+
+whff_status_t whff_dstream_destroy(whff_dstream_t s) {
+  free_stream(s);
+  return WHFF_OK;
+}
+
+whff_status_t whff_dstream_get_info(whff_dstream_t s, whff_dstream_info_t* info) {
+  if (!s || !info) return fail(WHFF_ERR_ARGUMENT, "null argument");
+  info->mode = s->mode;
+  info->index_kind = s->kind;
+  info->param = s->param;
+  info->rows = s->rows;
+  info->cols = s->cols;
+  info->n_blocks = s->nb;
+  info->payload_bytes = s->payload_bytes;
+  info->total_bits = s->total_bits ? s->total_bits : s->payload_bits;
+  info->index_bytes = s->index_bytes;
+  info->device_bytes = s->payload_alloc + s->index_bytes;
+  info->planes_limit = s->planes_limit;
+  info->has_raw_flag = s->has_raw;
+  return WHFF_OK;
+}
+
+whff_status_t whff_dstream_download(whff_dstream_t s, uint8_t* payload, uint64_t* index) {
+  if (!s) return fail(WHFF_ERR_ARGUMENT, "null stream");
+  DeviceGuard g(s->device);
+  if (payload && s->payload_bytes)
+    WCK(cudaMemcpy(payload, s->d_payload, s->payload_bytes, cudaMemcpyDeviceToHost));
+  if (index) {
+    if (s->kind == WHFF_INDEX_IMPLICIT) {
+      for (uint64_t b = 0; b < s->nb; ++b) index[b] = b * s->seg_bits;
+    } else if (s->kind == WHFF_INDEX_FULL) {
+      WCK(cudaMemcpy(index, s->d_starts, s->nb * 8, cudaMemcpyDeviceToHost));
+    } else {
+      std::vector<uint16_t> lens(s->nb);
+      std::vector<uint64_t> base(s->br * s->gpr);
+      WCK(cudaMemcpy(lens.data(), s->d_lens, s->nb * 2, cudaMemcpyDeviceToHost));
+      WCK(cudaMemcpy(base.data(), s->d_base, base.size() * 8, cudaMemcpyDeviceToHost));
+      for (uint64_t r = 0; r < s->br; ++r) {
+        for (uint64_t gg = 0; gg < s->gpr; ++gg) {
+          uint64_t st = base[r * s->gpr + gg];
+          for (uint64_t c = gg * 32; c < std::min<uint64_t>(s->bc, gg * 32 + 32); ++c) {
+            index[r * s->bc + c] = st;
+            st += lens[r * s->bc + c];
+          }
+        }
+      }
+    }
+  }
+  return WHFF_OK;
+}
+
+whff_status_t whff_compress(const float* a, uint64_t lda, uint64_t rows, uint64_t cols, int mode,
+                            double param, whff_stream_t stream, whff_dstream_t* out) {
+  if (!out) return fail(WHFF_ERR_ARGUMENT, "null output handle");
+  *out = nullptr;
+  whff_status_t st = check_mode(mode, param);
+  if (st != WHFF_OK) return st;
+  if (rows < 1 || cols < 1)
+    return fail(WHFF_ERR_DIMENSION, "codec input must be 2D and nonempty");
+  if (lda < cols) return fail(WHFF_ERR_DIMENSION, "lda < cols");
+  cudaStream_t cs = (cudaStream_t)stream;
+  int dev;
+  WCK(cudaGetDevice(&dev));
+  const uint64_t br = (rows + 3) / 4, bc = (cols + 3) / 4, nb = br * bc;
+  uint64_t *d_lens = nullptr, *d_off = nullptr;
+  int* d_ovf = nullptr;
+  void* d_tmp = nullptr;
+  size_t tmp_bytes = 0;
+  whff_dstream* s = nullptr;
+  whff_status_t rc = WHFF_OK;
+  uint64_t total = 0, last_len = 0, last_off = 0;
+  int ovf = 0;
+  cudaError_t e = cudaMalloc(&d_lens, nb * 8);
+  if (e == cudaSuccess) e = cudaMalloc(&d_off, nb * 8);
+  if (e == cudaSuccess) e = cudaMalloc(&d_ovf, sizeof(int));
+  if (e == cudaSuccess) e = cudaMemsetAsync(d_ovf, 0, sizeof(int), cs);
+  if (e != cudaSuccess) { rc = cuda_fail(e, "compress alloc"); goto done; }
+  k_encode_len<<<grid_for(nb, 128), 128, 0, cs>>>(a, lda, rows, cols, nb, bc, mode, param, d_lens, d_ovf);
+  e = cudaGetLastError();
+  if (e == cudaSuccess) e = cub::DeviceScan::ExclusiveSum(nullptr, tmp_bytes, d_lens, d_off, nb, cs);
+  if (e == cudaSuccess) e = cudaMalloc(&d_tmp, tmp_bytes);
+  if (e == cudaSuccess) e = cub::DeviceScan::ExclusiveSum(d_tmp, tmp_bytes, d_lens, d_off, nb, cs);
+  if (e == cudaSuccess) e = cudaMemcpyAsync(&last_len, d_lens + nb - 1, 8, cudaMemcpyDeviceToHost, cs);
+  if (e == cudaSuccess) e = cudaMemcpyAsync(&last_off, d_off + nb - 1, 8, cudaMemcpyDeviceToHost, cs);
+  if (e == cudaSuccess) e = cudaMemcpyAsync(&ovf, d_ovf, sizeof(int), cudaMemcpyDeviceToHost, cs);
+  if (e == cudaSuccess) e = cudaStreamSynchronize(cs);
+  if (e != cudaSuccess) { rc = cuda_fail(e, "compress pass 1"); goto done; }
+  if (ovf) { rc = fail(WHFF_ERR_OVERFLOW, "internal error: transform coefficient overflow"); goto done; }
+  total = last_off + last_len;
+  s = new whff_dstream();
+  s->device = dev;
+  s->mode = mode;
+  s->param = param;
+  s->rows = rows;
+  s->cols = cols;
+  s->br = br;
+  s->bc = bc;
+  s->nb = nb;
+  s->gpr = (bc + 31) / 32;
+  s->payload_bytes = (total + 7) / 8;
+  s->payload_bits = s->payload_bytes * 8;
+  s->total_bits = total;
+  s->planes_limit = planes_limit_for(mode, param);
+  s->has_raw = mode == WHFF_MODE_ACCURACY;
+  s->seg_bits = mode == WHFF_MODE_RATE ? (uint32_t)param * 16u : 0u;
+  rc = alloc_payload(s, s->payload_bytes);
+  if (rc != WHFF_OK) goto done;
+  k_encode_emit<<<grid_for(nb, 128), 128, 0, cs>>>(a, lda, rows, cols, nb, bc, mode, param, d_off,
+                                                   reinterpret_cast<uint32_t*>(s->d_payload));
+  e = cudaGetLastError();
+  if (e != cudaSuccess) { rc = cuda_fail(e, "compress pass 2"); goto done; }
+  if (mode == WHFF_MODE_RATE) {
+    s->kind = WHFF_INDEX_IMPLICIT;
+  } else {
+    s->kind = WHFF_INDEX_COMPACT;  // encoder segments are <= 1333 bits
+    e = cudaMalloc(&s->d_lens, nb * 2);
+    if (e == cudaSuccess) e = cudaMalloc(&s->d_base, br * s->gpr * 8);
+    if (e != cudaSuccess) { rc = cuda_fail(e, "compress index alloc"); goto done; }
+    k_build_compact<<<grid_for(nb, 256), 256, 0, cs>>>(d_off, nb, bc, s->gpr, s->payload_bits,
+                                                       s->d_lens, s->d_base);
+    s->index_bytes = nb * 2 + br * s->gpr * 8;
+  }
+  e = cudaStreamSynchronize(cs);
+  if (e != cudaSuccess) { rc = cuda_fail(e, "compress finish"); goto done; }
+done:
+  cudaFree(d_lens);
+  cudaFree(d_off);
+  cudaFree(d_ovf);
+  cudaFree(d_tmp);
+  if (rc != WHFF_OK) {
+    free_stream(s);
+    return rc;
+  }
+  *out = s;
+  return WHFF_OK;
+}
+
+static EncArrays enc_arrays(const uint32_t* mag, const uint8_t* neg, const uint16_t* emax,
+                            const uint8_t* planes, const uint8_t* raw_mask, const uint32_t* raw_words) {
+  EncArrays E{mag, neg, emax, planes, raw_mask, raw_words};
+  return E;
+}
+
+whff_status_t whff_encode_blocks_size(const uint32_t* mag, const uint8_t* neg, const uint16_t* emax,
+                                      const uint8_t* planes, const uint8_t* raw_mask,
+                                      const uint32_t* raw_words, uint64_t nb, int n_planes,
+                                      int budget_bits, int has_raw, uint64_t* offsets,
+                                      uint64_t* total_bits, whff_stream_t stream) {
+  if (n_planes != kNPlanes) return fail(WHFF_ERR_ARGUMENT, "n_planes must be 27");
+  if (!total_bits) return fail(WHFF_ERR_ARGUMENT, "null total_bits");
+  *total_bits = 0;
+  if (nb == 0) return WHFF_OK;
+  cudaStream_t cs = (cudaStream_t)stream;
+  uint64_t* d_lens = nullptr;
+  void* d_tmp = nullptr;
+  size_t tmp_bytes = 0;
+  uint64_t last_len = 0, last_off = 0;
+  cudaError_t e = cudaMalloc(&d_lens, nb * 8);
+  if (e == cudaSuccess) {
+    k_encblocks_len<<<grid_for(nb, 128), 128, 0, cs>>>(
+        enc_arrays(mag, neg, emax, planes, raw_mask, raw_words), nb, budget_bits, has_raw, d_lens);
+    e = cudaGetLastError();
+  }
+  if (e == cudaSuccess) e = cub::DeviceScan::ExclusiveSum(nullptr, tmp_bytes, d_lens, offsets, nb, cs);
+  if (e == cudaSuccess) e = cudaMalloc(&d_tmp, tmp_bytes);
+  if (e == cudaSuccess) e = cub::DeviceScan::ExclusiveSum(d_tmp, tmp_bytes, d_lens, offsets, nb, cs);
+  if (e == cudaSuccess) e = cudaMemcpyAsync(&last_len, d_lens + nb - 1, 8, cudaMemcpyDeviceToHost, cs);
+  if (e == cudaSuccess) e = cudaMemcpyAsync(&last_off, offsets + nb - 1, 8, cudaMemcpyDeviceToHost, cs);
+  if (e == cudaSuccess) e = cudaStreamSynchronize(cs);
+  cudaFree(d_lens);
+  cudaFree(d_tmp);
+  if (e != cudaSuccess) return cuda_fail(e, "encode_blocks pass 1");
+  *total_bits = last_off + last_len;
+  return WHFF_OK;
+}
+
+whff_status_t whff_encode_blocks_emit(const uint32_t* mag, const uint8_t* neg, const uint16_t* emax,
+                                      const uint8_t* planes, const uint8_t* raw_mask,
+                                      const uint32_t* raw_words, uint64_t nb, int n_planes,
+                                      int budget_bits, int has_raw, const uint64_t* offsets,
+                                      uint8_t* payload, whff_stream_t stream) {
+  if (n_planes != kNPlanes) return fail(WHFF_ERR_ARGUMENT, "n_planes must be 27");
+  if (nb == 0) return WHFF_OK;
+  if ((reinterpret_cast<uintptr_t>(payload) & 3u) != 0)
+    return fail(WHFF_ERR_ARGUMENT, "payload must be 4-byte aligned");
+  k_encblocks_emit<<<grid_for(nb, 128), 128, 0, (cudaStream_t)stream>>>(
+      enc_arrays(mag, neg, emax, planes, raw_mask, raw_words), nb, budget_bits, has_raw, offsets,
+      reinterpret_cast<uint32_t*>(payload));
+  WCK_LAUNCH("encode_blocks pass 2");
+  return WHFF_OK;
+}
+
+whff_status_t whff_decode_blocks(whff_dstream_t s, uint64_t first, uint64_t count, int planes_limit,
+                                 uint32_t* mag, uint8_t* neg, uint16_t* emax, uint8_t* raw,
+                                 uint32_t* raw_words, uint64_t* consumed, whff_stream_t stream) {
+  if (!s) return fail(WHFF_ERR_ARGUMENT, "null stream");
+  if (first > s->nb || count > s->nb - first) return fail(WHFF_ERR_CORRUPT, "block index out of range");
+  if (count == 0) return WHFF_OK;
+  const int pl = planes_limit < 0 ? s->planes_limit : std::min(planes_limit, kNPlanes);
+  const StreamView v = s->view();
+  cudaStream_t cs = (cudaStream_t)stream;
+  if (s->has_raw)
+    k_decode_blocks<true><<<grid_for(count, 128), 128, 0, cs>>>(v, first, count, pl, mag, neg, emax,
+                                                               raw, raw_words, consumed);
+  else
+    k_decode_blocks<false><<<grid_for(count, 128), 128, 0, cs>>>(v, first, count, pl, mag, neg, emax,
+                                                                raw, raw_words, consumed);
+  WCK_LAUNCH("decode_blocks");
+  return WHFF_OK;
+}
+
+whff_status_t whff_decode_block_words(whff_dstream_t s, uint64_t first, uint64_t count, float* out,
+                                      whff_stream_t stream) {
+  if (!s || !out) return fail(WHFF_ERR_ARGUMENT, "null argument");
+  if (first > s->nb || count > s->nb - first) return fail(WHFF_ERR_CORRUPT, "block index out of range");
+  if (count == 0) return WHFF_OK;
+  const StreamView v = s->view();
+  cudaStream_t cs = (cudaStream_t)stream;
+  if (s->has_raw)
+    k_decode_block_words<true><<<grid_for(count, 128), 128, 0, cs>>>(v, first, count, out);
+  else
+    k_decode_block_words<false><<<grid_for(count, 128), 128, 0, cs>>>(v, first, count, out);
+  WCK_LAUNCH("decode_block_words");
+  return WHFF_OK;
+}
+
+whff_status_t whff_decode(whff_dstream_t s, float* out, uint64_t ld, uint64_t* status,
+                          whff_stream_t stream) {
+  if (!s || !out || !status) return fail(WHFF_ERR_ARGUMENT, "null argument");
+  if (ld < s->cols) return fail(WHFF_ERR_DIMENSION, "ld_out < cols");
+  const StreamView v = s->view();
+  cudaStream_t cs = (cudaStream_t)stream;
+  auto* st = reinterpret_cast<unsigned long long*>(status);
+  if (s->has_raw)
+    k_decode_words<true><<<grid_for(s->nb, 128), 128, 0, cs>>>(v, out, ld, st);
+  else
+    k_decode_words<false><<<grid_for(s->nb, 128), 128, 0, cs>>>(v, out, ld, st);
+  WCK_LAUNCH("decode");
+  return WHFF_OK;
+}
+
+}  // extern "C"
+
+// ---- fused decode + GEMV -------------------------------------------------
+
+static int variant_of(const whff_dstream* s) {
+  if (s->kind == WHFF_INDEX_IMPLICIT) return s->seg_bits == 128 ? 0 : 1;
+  return s->has_raw ? 3 : 2;
+}
+
+template <int EVAL>
+static whff_status_t launch_gemv_var(int var, const JobTable& T, int policy,
+                                     unsigned long long* status, cudaStream_t cs) {
+  const unsigned threads = 256;
+  const unsigned blocks = grid_for(T.total_warps * 32, threads);
+  if (blocks == 0) return WHFF_OK;
+  switch (var) {
+    case 0: k_decode_gemv<0, EVAL><<<blocks, threads, 0, cs>>>(T, policy, status); break;
+    case 1: k_decode_gemv<1, EVAL><<<blocks, threads, 0, cs>>>(T, policy, status); break;
+    case 2: k_decode_gemv<2, EVAL><<<blocks, threads, 0, cs>>>(T, policy, status); break;
+    default: k_decode_gemv<3, EVAL><<<blocks, threads, 0, cs>>>(T, policy, status); break;
+  }
+  WCK_LAUNCH("decode_gemv");
+  return WHFF_OK;
+}
+
+static whff_status_t launch_gemv(int var, int eval, const JobTable& T, int policy,
+                                 unsigned long long* status, cudaStream_t cs) {
+  if (eval == WHFF_EVAL_COEFF) return launch_gemv_var<WHFF_EVAL_COEFF>(var, T, policy, status, cs);
+  return launch_gemv_var<WHFF_EVAL_EXACT>(var, T, policy, status, cs);
+}
+
+extern "C" whff_status_t whff_decode_gemv_workspace_size(whff_dstream_t s, int eval, size_t* bytes) {
+  if (!s || !bytes) return fail(WHFF_ERR_ARGUMENT, "null argument");
+  *bytes = eval == WHFF_EVAL_COEFF ? s->bc * sizeof(float4) : 0;
+  return WHFF_OK;
+}
+
+static whff_status_t check_policy_eval(int policy, int eval) {
+  if (policy < 0 || policy > 2) return fail(WHFF_ERR_ARGUMENT, "unknown precision policy");
+  if (eval < 0 || eval > 1) return fail(WHFF_ERR_ARGUMENT, "unknown evaluation");
+  if (eval == WHFF_EVAL_COEFF && policy == WHFF_POLICY_DOUBLE)
+    return fail(WHFF_ERR_ARGUMENT, "coefficient evaluation supports mixed and single only");
+  return WHFF_OK;
+}
+
+extern "C" whff_status_t whff_decode_gemv(whff_dstream_t s, const float* v, float* y, int policy, int eval,
+                               uint64_t row_begin, uint64_t row_end, void* ws, size_t ws_bytes,
+                               uint64_t* status, whff_stream_t stream) {
+  if (!s || !v || !y || !status) return fail(WHFF_ERR_ARGUMENT, "null argument");
+  whff_status_t st = check_policy_eval(policy, eval);
+  if (st != WHFF_OK) return st;
+  if (row_begin > row_end || row_end > s->rows) return fail(WHFF_ERR_DIMENSION, "bad row range");
+  if (row_begin == row_end) return WHFF_OK;
+  cudaStream_t cs = (cudaStream_t)stream;
+  JobTable T;
+  T.jobs = nullptr;
+  T.prefix = nullptr;
+  T.n = 1;
+  T.single.s = s->view();
+  T.single.v = v;
+  T.single.y = y;
+  T.single.U = nullptr;
+  T.single.row_begin = row_begin;
+  T.single.row_end = row_end;
+  T.single.br0 = row_begin / 4;
+  T.total_warps = (row_end + 3) / 4 - row_begin / 4;
+  if (eval == WHFF_EVAL_COEFF) {
+    if (!ws || ws_bytes < s->bc * sizeof(float4)) return fail(WHFF_ERR_ARGUMENT, "workspace too small");
+    if ((reinterpret_cast<uintptr_t>(ws) & 15u) != 0) return fail(WHFF_ERR_ARGUMENT, "workspace alignment");
+    k_coeff_prep<<<grid_for(s->bc, 256), 256, 0, cs>>>(v, s->cols, s->bc, reinterpret_cast<float4*>(ws));
+    WCK_LAUNCH("coeff_prep");
+    T.single.U = reinterpret_cast<const float4*>(ws);
+  }
+  return launch_gemv(variant_of(s), eval, T, policy, reinterpret_cast<unsigned long long*>(status), cs);
+}
+
+struct whff_gemv_plan {
+  int device = 0;
+  int n = 0;
+  int policy = 0, eval = 0, var = 0;
+  GemvJob* d_jobs = nullptr;
+  uint64_t* d_prefix = nullptr;
+  uint64_t total_warps = 0;
+  float4* d_U = nullptr;
+  // distinct vectors for the coefficient prologue
+  std::vector<const float*> prep_v;
+  std::vector<uint64_t> prep_cols, prep_bc, prep_off;
+  uint64_t bytes_read = 0, bytes_written = 0, n_blocks = 0;
+};
+
+extern "C" {
+
+whff_status_t whff_gemv_plan_create(int n, const whff_dstream_t* streams, const float* const* v,
+                                    float* const* y, const uint64_t* rb, const uint64_t* re,
+                                    int policy, int eval, whff_gemv_plan_t* out) {
+  if (!out || n < 1 || !streams || !v || !y || !rb || !re) return fail(WHFF_ERR_ARGUMENT, "bad plan arguments");
+  *out = nullptr;
+  whff_status_t st = check_policy_eval(policy, eval);
+  if (st != WHFF_OK) return st;
+  const int var = variant_of(streams[0]);
+  for (int i = 0; i < n; ++i) {
+    if (!streams[i] || variant_of(streams[i]) != var || streams[i]->mode != streams[0]->mode)
+      return fail(WHFF_ERR_ARGUMENT, "plan streams must share mode and index kind");
+    if (rb[i] > re[i] || re[i] > streams[i]->rows) return fail(WHFF_ERR_DIMENSION, "bad row range");
+  }
+  whff_gemv_plan* P = new whff_gemv_plan();
+  cudaGetDevice(&P->device);
+  P->n = n;
+  P->policy = policy;
+  P->eval = eval;
+  P->var = var;
+  std::vector<GemvJob> jobs(n);
+  std::vector<uint64_t> prefix(n), uoff(n, 0);
+  uint64_t warps = 0, ucount = 0;
+  for (int i = 0; i < n; ++i) {
+    const whff_dstream* s = streams[i];
+    GemvJob& J = jobs[i];
+    J.s = s->view();
+    J.v = v[i];
+    J.y = y[i];
+    J.U = nullptr;
+    J.row_begin = rb[i];
+    J.row_end = re[i];
+    J.br0 = rb[i] / 4;
+    prefix[i] = warps;
+    const uint64_t nbr = rb[i] == re[i] ? 0 : (re[i] + 3) / 4 - rb[i] / 4;
+    warps += nbr;
+    // traffic accounting (roofline): payload + index of the covered rows
+    const uint64_t blocks = nbr * s->bc;
+    P->n_blocks += blocks;
+    if (s->kind == WHFF_INDEX_IMPLICIT)
+      P->bytes_read += blocks * s->seg_bits / 8;
+    else
+      P->bytes_read += (uint64_t)((double)s->payload_bytes * blocks / std::max<uint64_t>(s->nb, 1));
+    P->bytes_read += (uint64_t)((double)s->index_bytes * blocks / std::max<uint64_t>(s->nb, 1));
+    P->bytes_written += (re[i] - rb[i]) * 4;
+    // distinct vectors
+    int found = -1;
+    for (size_t k = 0; k < P->prep_v.size(); ++k)
+      if (P->prep_v[k] == v[i] && P->prep_cols[k] == s->cols) found = (int)k;
+    if (found < 0) {
+      P->prep_v.push_back(v[i]);
+      P->prep_cols.push_back(s->cols);
+      P->prep_bc.push_back(s->bc);
+      P->prep_off.push_back(ucount);
+      ucount += s->bc;
+      P->bytes_read += s->cols * 4;
+      found = (int)P->prep_v.size() - 1;
+    }
+    uoff[i] = P->prep_off[found];
+  }
+  P->total_warps = warps;
+  cudaError_t e = cudaSuccess;
+  if (eval == WHFF_EVAL_COEFF) {
+    e = cudaMalloc(&P->d_U, std::max<uint64_t>(ucount, 1) * sizeof(float4));
+    for (int i = 0; i < n && e == cudaSuccess; ++i) jobs[i].U = P->d_U + uoff[i];
+  }
+  if (e == cudaSuccess) e = cudaMalloc(&P->d_jobs, n * sizeof(GemvJob));
+  if (e == cudaSuccess) e = cudaMalloc(&P->d_prefix, n * sizeof(uint64_t));
+  if (e == cudaSuccess) e = cudaMemcpy(P->d_jobs, jobs.data(), n * sizeof(GemvJob), cudaMemcpyHostToDevice);
+  if (e == cudaSuccess) e = cudaMemcpy(P->d_prefix, prefix.data(), n * 8, cudaMemcpyHostToDevice);
+  if (e != cudaSuccess) {
+    cudaFree(P->d_U);
+    cudaFree(P->d_jobs);
+    cudaFree(P->d_prefix);
+    delete P;
+    return cuda_fail(e, "plan create");
+  }
+  *out = P;
+  return WHFF_OK;
+}
+
+whff_status_t whff_gemv_plan_launch(whff_gemv_plan_t P, uint64_t* status, whff_stream_t stream) {
+  if (!P || !status) return fail(WHFF_ERR_ARGUMENT, "null argument");
+  cudaStream_t cs = (cudaStream_t)stream;
+  if (P->eval == WHFF_EVAL_COEFF) {
+    for (size_t k = 0; k < P->prep_v.size(); ++k) {
+      k_coeff_prep<<<grid_for(P->prep_bc[k], 256), 256, 0, cs>>>(P->prep_v[k], P->prep_cols[k],
+                                                                 P->prep_bc[k], P->d_U + P->prep_off[k]);
+    }
+    WCK_LAUNCH("plan coeff_prep");
+  }
+  JobTable T;
+  T.jobs = P->d_jobs;
+  T.prefix = P->d_prefix;
+  T.n = P->n;
+  T.total_warps = P->total_warps;
+  memset(&T.single, 0, sizeof(T.single));
+  return launch_gemv(P->var, P->eval, T, P->policy, reinterpret_cast<unsigned long long*>(status), cs);
+}
+
+whff_status_t whff_gemv_plan_traffic(whff_gemv_plan_t P, uint64_t* br, uint64_t* bw, uint64_t* nb) {
+  if (!P) return fail(WHFF_ERR_ARGUMENT, "null plan");
+  if (br) *br = P->bytes_read;
+  if (bw) *bw = P->bytes_written;
+  if (nb) *nb = P->n_blocks;
+  return WHFF_OK;
+}
+
+whff_status_t whff_gemv_plan_destroy(whff_gemv_plan_t P) {
+  if (!P) return WHFF_OK;
+  DeviceGuard g(P->device);
+  cudaFree(P->d_U);
+  cudaFree(P->d_jobs);
+  cudaFree(P->d_prefix);
+  delete P;
+  return WHFF_OK;
+}
+
+}  // extern "C"
+
+// ---- dense GEMV -----------------------------------------------------------
+
+static void blocked_split(uint64_t rows, uint64_t cols, uint64_t& nseg, uint64_t& seg_cols) {
+  // enough warps to fill 148 SMs x 16 warps, segments a multiple of 128 cols
+  const uint64_t target = 148ull * 16;
+  nseg = rows >= target ? 1 : (target + rows - 1) / rows;
+  const uint64_t max_seg = std::max<uint64_t>(1, (cols + 127) / 128);
+  nseg = std::min(nseg, max_seg);
+  seg_cols = ((cols + nseg - 1) / nseg + 127) / 128 * 128;
+  nseg = (cols + seg_cols - 1) / seg_cols;
+  if (nseg == 0) nseg = 1;
+}
+
+extern "C" whff_status_t whff_gemv_workspace_size(uint64_t rows, uint64_t cols, int policy, int shape, int fanout,
+                                       size_t* bytes) {
+  if (!bytes) return fail(WHFF_ERR_ARGUMENT, "null argument");
+  *bytes = 0;
+  if (shape == WHFF_SHAPE_FIXED_TREE) {
+    if (fanout < 2 || (fanout & (fanout - 1))) return fail(WHFF_ERR_ARGUMENT, "tree fanout must be a power of two >= 2");
+    const uint64_t ng = (cols + fanout - 1) / fanout;
+    const size_t el = policy == WHFF_POLICY_SINGLE ? 4 : 8;
+    *bytes = 2 * rows * std::max<uint64_t>(ng, 1) * el + 256;
+  } else if (shape == WHFF_SHAPE_BLOCKED) {
+    uint64_t nseg, segc;
+    blocked_split(rows, cols, nseg, segc);
+    *bytes = rows * nseg * 8;
+  }
+  return WHFF_OK;
+}
+
+template <int POL>
+static whff_status_t gemv_pol(const float* A, uint64_t lda, uint64_t rows, uint64_t cols,
+                              const float* v, float* y, int shape, int fanout, void* ws, size_t wsb,
+                              cudaStream_t cs) {
+  if (shape == WHFF_SHAPE_SEQUENTIAL) {
+    k_gemv_seq<POL, false><<<grid_for(rows, 64), 64, 0, cs>>>(A, lda, rows, cols, v, y, nullptr);
+    WCK_LAUNCH("gemv sequential");
+    return WHFF_OK;
+  }
+  size_t need = 0;
+  whff_status_t st = whff_gemv_workspace_size(rows, cols, POL, shape, fanout, &need);
+  if (st != WHFF_OK) return st;
+  if (wsb < need || (need && !ws)) return fail(WHFF_ERR_ARGUMENT, "workspace too small");
+  if (shape == WHFF_SHAPE_FIXED_TREE) {
+    using T = typename std::conditional<POL == WHFF_POLICY_SINGLE, float, double>::type;
+    T* b0 = reinterpret_cast<T*>(ws);
+    uint64_t ng = (cols + fanout - 1) / fanout;
+    T* b1 = b0 + rows * std::max<uint64_t>(ng, 1);
+    k_gemv_tree_leaf<POL, T><<<grid_for(rows * ng, 256), 256, 0, cs>>>(A, lda, rows, cols, v, fanout, b0, ng);
+    WCK_LAUNCH("gemv tree leaf");
+    uint64_t w = ng;
+    while (w > 1) {
+      const uint64_t n2 = (w + fanout - 1) / fanout;
+      k_gemv_tree_level<T><<<grid_for(rows * n2, 256), 256, 0, cs>>>(b0, rows, w, fanout, b1, n2);
+      WCK_LAUNCH("gemv tree level");
+      std::swap(b0, b1);
+      w = n2;
+    }
+    k_tree_store<T><<<grid_for(rows, 256), 256, 0, cs>>>(b0, rows, y);
+    WCK_LAUNCH("gemv tree store");
+    return WHFF_OK;
+  }
+  if (shape != WHFF_SHAPE_BLOCKED) return fail(WHFF_ERR_ARGUMENT, "unknown reduction shape");
+  uint64_t nseg, segc;
+  blocked_split(rows, cols, nseg, segc);
+  const bool vec4 = (lda % 4 == 0) && ((reinterpret_cast<uintptr_t>(A) & 15u) == 0) &&
+                    ((reinterpret_cast<uintptr_t>(v) & 15u) == 0);
+  k_gemv_blocked<POL><<<grid_for(rows * nseg * 32, 256), 256, 0, cs>>>(
+      A, lda, rows, cols, v, nseg, segc, vec4, reinterpret_cast<double*>(ws));
+  WCK_LAUNCH("gemv blocked");
+  k_blocked_finish<POL><<<grid_for(rows, 256), 256, 0, cs>>>(reinterpret_cast<double*>(ws), rows, nseg, y);
+  WCK_LAUNCH("gemv blocked finish");
+  return WHFF_OK;
+}
+
+extern "C" {
+
+whff_status_t whff_gemv(const float* A, uint64_t lda, uint64_t rows, uint64_t cols, const float* v,
+                        float* y, int policy, int shape, int fanout, void* ws, size_t wsb,
+                        whff_stream_t stream) {
+  if (!A || !v || !y) return fail(WHFF_ERR_ARGUMENT, "null argument");
+  if (rows < 1 || cols < 1) return fail(WHFF_ERR_DIMENSION, "gemv operands must be nonempty");
+  if (lda < cols) return fail(WHFF_ERR_DIMENSION, "lda < cols");
+  cudaStream_t cs = (cudaStream_t)stream;
+  switch (policy) {
+    case WHFF_POLICY_MIXED: return gemv_pol<WHFF_POLICY_MIXED>(A, lda, rows, cols, v, y, shape, fanout, ws, wsb, cs);
+    case WHFF_POLICY_SINGLE: return gemv_pol<WHFF_POLICY_SINGLE>(A, lda, rows, cols, v, y, shape, fanout, ws, wsb, cs);
+    case WHFF_POLICY_DOUBLE: return gemv_pol<WHFF_POLICY_DOUBLE>(A, lda, rows, cols, v, y, shape, fanout, ws, wsb, cs);
+  }
+  return fail(WHFF_ERR_ARGUMENT, "unknown precision policy");
+}
+
+whff_status_t whff_gemv_oracle(const float* A, uint64_t lda, uint64_t rows, uint64_t cols,
+                               const float* v, double* y, whff_stream_t stream) {
+  if (!A || !v || !y) return fail(WHFF_ERR_ARGUMENT, "null argument");
+  if (rows < 1 || cols < 1) return fail(WHFF_ERR_DIMENSION, "gemv operands must be nonempty");
+  k_gemv_seq<WHFF_POLICY_DOUBLE, true><<<grid_for(rows, 64), 64, 0, (cudaStream_t)stream>>>(
+      A, lda, rows, cols, v, nullptr, y);
+  WCK_LAUNCH("gemv oracle");
+  return WHFF_OK;
+}
+
+whff_status_t whff_find_nonfinite(const float* x, uint64_t n, uint64_t* status, whff_stream_t stream) {
+  if (!status) return fail(WHFF_ERR_ARGUMENT, "null status");
+  if (n == 0) return WHFF_OK;
+  const unsigned blocks = (unsigned)std::min<uint64_t>(grid_for(n, 256), 148ull * 8);
+  k_find_nonfinite<<<blocks, 256, 0, (cudaStream_t)stream>>>(x, n, reinterpret_cast<unsigned long long*>(status));
+  WCK_LAUNCH("find_nonfinite");
+  return WHFF_OK;
+}
+
+whff_status_t whff_csr_matvec(const int64_t* indptr, const int32_t* indices, const double* data,
+                              uint64_t n, const float* x, const float* b, const float* u, float* y,
+                              whff_stream_t stream) {
+  if (!indptr || !x || !y) return fail(WHFF_ERR_ARGUMENT, "null argument");
+  if ((b == nullptr) != (u == nullptr)) return fail(WHFF_ERR_ARGUMENT, "b and u go together");
+  if (n == 0) return WHFF_OK;
+  k_csr_matvec<<<grid_for(n, 256), 256, 0, (cudaStream_t)stream>>>(indptr, indices, data, n, x, b, u, y);
+  WCK_LAUNCH("csr_matvec");
+  return WHFF_OK;
+}
+
+whff_status_t whff_source_term(const float* fp, const float* dark, float dose, uint64_t n, float* u,
+                               whff_stream_t stream) {
+  if (!dark || !u) return fail(WHFF_ERR_ARGUMENT, "null argument");
+  if (n == 0) return WHFF_OK;
+  k_source_term<<<grid_for(n, 256), 256, 0, (cudaStream_t)stream>>>(fp, dark, dose, n, u);
+  WCK_LAUNCH("source_term");
+  return WHFF_OK;
+}
+
+}  // extern "C"

@@ -1,0 +1,134 @@
+"""Per-millisecond thermal update on the B200 (thermal.py:81-140 of the
+reference): T_{k+1} = fp32(A64 T_k + B u_k), S_{k+1} = fp32(P64 T_{k+1}).
+
+CSR values are widened to binary64 once (thermal.py:101-102) and each row is
+accumulated in CSR order like scipy's csr_matvec, so results are bit-identical
+to the reference (tests/test_thermal_gpu.py).  numpy in -> numpy out, CUDA
+tensors in -> CUDA tensors out.
+"""
+
+from __future__ import annotations
+
+from dataclasses import dataclass
+
+import numpy as np
+
+from . import _lib
+from .errors import DimensionError, NonFiniteError, WhffError
+
+
+class DeviceCSR:
+    """CSR operator resident on the device with binary64 values."""
+
+    def __init__(self, matrix, device="cuda"):
+        torch = _lib.require_cuda()
+        if isinstance(matrix, DeviceCSR):
+            self.__dict__.update(matrix.__dict__)
+            return
+        m = matrix.tocsr()
+        self.shape = m.shape
+        self.nnz = int(m.nnz)
+        self.indptr = torch.from_numpy(np.ascontiguousarray(m.indptr, np.int64)).to(device)
+        self.indices = torch.from_numpy(np.ascontiguousarray(m.indices, np.int32)).to(device)
+        self.data = torch.from_numpy(np.ascontiguousarray(m.data, np.float64)).to(device)
+
+    @property
+    def bytes(self):
+        return self.indptr.numel() * 8 + self.indices.numel() * 4 + self.data.numel() * 8
+
+
+def _dev_vec(x):
+    torch = _lib.require_cuda()
+    if isinstance(x, torch.Tensor):
+        return x.to(device="cuda", dtype=torch.float32).contiguous(), True
+    return torch.from_numpy(np.ascontiguousarray(x, dtype=np.float32)).cuda(), False
+
+
+def _check_vector(name, v, n):
+    """thermal.py:91-95."""
+    from .codec import find_nonfinite
+    if tuple(v.shape) != (n,):
+        raise DimensionError(f"{name} has shape {tuple(v.shape)}, expected ({n},)")
+    bad = find_nonfinite(v)
+    if bad is not None:
+        raise NonFiniteError(name, bad)
+
+
+def csr_matvec(A, x, b=None, u=None, out=None):
+    """y = fp32(A64 x [+ b*u]) on device tensors, no checks (hot path)."""
+    torch = _lib.require_cuda()
+    if out is None:
+        out = torch.empty(A.shape[0], dtype=torch.float32, device=x.device)
+    _lib.call("whff_csr_matvec", _lib.ptr(A.indptr), _lib.ptr(A.indices), _lib.ptr(A.data),
+              A.shape[0], _lib.ptr(x), _lib.ptr(b), _lib.ptr(u), _lib.ptr(out), _lib.cur_stream())
+    return out
+
+
+def thermal_step(A64, B, T_k, u_k):
+    """thermal.py:98-109."""
+    A = A64 if isinstance(A64, DeviceCSR) else DeviceCSR(A64)
+    n = A.shape[0]
+    t, dev = _dev_vec(T_k)
+    u, _ = _dev_vec(u_k)
+    b, _ = _dev_vec(B)
+    _check_vector("T_k", t, n)
+    _check_vector("u_k", u, n)
+    y = csr_matvec(A, t, b, u)
+    return y if dev else y.cpu().numpy()
+
+
+def thermal_interpolate(P64, T_next):
+    """thermal.py:112-117."""
+    P = P64 if isinstance(P64, DeviceCSR) else DeviceCSR(P64)
+    t, dev = _dev_vec(T_next)
+    if P.shape[1] != t.shape[0]:
+        raise DimensionError(
+            f"interpolation shapes differ: P is {P.shape}, T is {tuple(t.shape)}")
+    y = csr_matvec(P, t)
+    return y if dev else y.cpu().numpy()
+
+
+def source_term_device(footprint, dark, dose, out=None):
+    """thermal.py:81-88: u = fp32(dose) * footprint + dark (dark step: footprint None)."""
+    torch = _lib.require_cuda()
+    if out is None:
+        out = torch.empty_like(dark)
+    _lib.call("whff_source_term", _lib.ptr(footprint), _lib.ptr(dark), float(np.float32(dose)),
+              dark.numel(), _lib.ptr(out), _lib.cur_stream())
+    return out
+
+
+@dataclass
+class ThermalState:
+    """thermal.py:18-28, device resident."""
+    k: int
+    temperatures: object      # (T,) float32 CUDA tensor
+    interpolated: object      # (S,) float32 CUDA tensor
+
+    @classmethod
+    def initial(cls, T, S):
+        torch = _lib.require_cuda()
+        return cls(0, torch.zeros(T, dtype=torch.float32, device="cuda"),
+                   torch.zeros(S, dtype=torch.float32, device="cuda"))
+
+
+class DeviceHeatLoad:
+    """Device copy of a reference HeatLoad (thermal.py:31-59)."""
+
+    def __init__(self, dark_load, light_footprints, dose_scale=1.0):
+        torch = _lib.require_cuda()
+        self.dark = torch.from_numpy(np.ascontiguousarray(dark_load, np.float32)).cuda()
+        self.footprints = {k: torch.from_numpy(np.ascontiguousarray(v, np.float32)).cuda()
+                           for k, v in light_footprints.items()}
+        self.dose_scale = float(dose_scale)
+
+    def source(self, field_id, phase, slit_id=None, out=None):
+        if phase == "dark":
+            return source_term_device(None, self.dark, 0.0, out)
+        if phase != "light":
+            raise WhffError(f"step phase must be light or dark, got {phase!r}")
+        try:
+            fp = self.footprints[(field_id, slit_id)]
+        except KeyError:
+            raise WhffError(f"no light footprint for field {field_id} slit {slit_id}") from None
+        return source_term_device(fp, self.dark, self.dose_scale, out)

@@ -1,0 +1,105 @@
+// Host build of the device decoder (paper_1902_08018_b200/csrc/whff_decode.cuh)
+// so its exact logic can be compared with the CPU oracle without a GPU.
+// Built by tests/conftest.py into tools/libhostcheck.so (test-only).
+#include <cstring>
+#include "../paper_1902_08018_b200/csrc/whff_decode.cuh"
+
+extern "C" {
+
+// words: payload as little-endian uint32 words, zero padded (>= 8 words).
+void hc_decode_blocks(const uint32_t* words, uint64_t payload_bits,
+                      const uint64_t* offsets, const uint64_t* seglens,
+                      int64_t nb, int planes_limit, int has_raw,
+                      uint32_t* mag, uint8_t* neg, uint16_t* emax, uint8_t* raw,
+                      uint32_t* raw_words, uint64_t* consumed) {
+  for (int64_t b = 0; b < nb; ++b) {
+    uint64_t start = offsets[b];
+    uint64_t limit = start + seglens[b];
+    if (limit > payload_bits) limit = payload_bits;
+    int64_t len64 = (int64_t)limit - (int64_t)start;
+    int len = len64 > 65535 ? 65535 : (int)len64;
+    whff::BitWindow bw;
+    whff::window_at(bw, words, start);
+    whff::Decoded d;
+    if (has_raw)
+      whff::decode_block<true, true>(bw, len, planes_limit, d);
+    else
+      whff::decode_block<false, true>(bw, len, planes_limit, d);
+    emax[b] = (uint16_t)d.emax;
+    raw[b] = (uint8_t)d.raw;
+    consumed[b] = (uint64_t)d.consumed;
+    for (int c = 0; c < 16; ++c) {
+      if (d.raw) {
+        raw_words[16 * b + c] = d.mag[c];
+        mag[16 * b + c] = 0;
+      } else {
+        mag[16 * b + c] = d.mag[c];
+        raw_words[16 * b + c] = 0;
+      }
+      neg[16 * b + c] = (uint8_t)((d.negm >> c) & 1u);
+    }
+  }
+}
+
+// Full decode into a (rows, cols) float32 array (codec.decompress sans checks).
+void hc_decompress(const uint32_t* words, uint64_t payload_bits,
+                   const uint64_t* offsets, const uint64_t* seglens,
+                   int64_t rows, int64_t cols, int planes_limit, int has_raw,
+                   float* out) {
+  int64_t bc = (cols + 3) / 4, br = (rows + 3) / 4;
+  for (int64_t b = 0; b < br * bc; ++b) {
+    uint64_t start = offsets[b];
+    uint64_t limit = start + seglens[b];
+    if (limit > payload_bits) limit = payload_bits;
+    int64_t len64 = (int64_t)limit - (int64_t)start;
+    int len = len64 > 65535 ? 65535 : (int)len64;
+    whff::BitWindow bw;
+    whff::window_at(bw, words, start);
+    whff::Decoded d;
+    if (has_raw)
+      whff::decode_block<true, true>(bw, len, planes_limit, d);
+    else
+      whff::decode_block<false, true>(bw, len, planes_limit, d);
+    float blk[16];
+    whff::reconstruct_words(d, blk);
+    int64_t r0 = (b / bc) * 4, c0 = (b % bc) * 4;
+    for (int i = 0; i < 4; ++i)
+      for (int j = 0; j < 4; ++j)
+        if (r0 + i < rows && c0 + j < cols) out[(r0 + i) * cols + c0 + j] = blk[4 * i + j];
+  }
+}
+
+}  // extern "C"
+
+#include "../paper_1902_08018_b200/csrc/whff_encode.cuh"
+extern "C" {
+// Two-pass GPU-encoder logic on the host: returns total bits, fills offsets;
+// when words != NULL also emits the payload (LE uint32 words, zeroed).
+int64_t hc_compress(const float* a, int64_t rows, int64_t cols, int mode, double param,
+                    uint64_t* offsets, uint32_t* words) {
+  int64_t br = (rows + 3) / 4, bc = (cols + 3) / 4, nb = br * bc;
+  int budget = mode == 0 ? (int)param * 16 : 0;
+  bool has_raw = mode == 2;
+  uint64_t total = 0;
+  for (int64_t b = 0; b < nb; ++b) {
+    whff::BlockPlan pl;
+    whff::plan_block(a, cols, rows, cols, b, bc, mode, param, pl);
+    if (!pl.ok) return -1;
+    offsets[b] = total;
+    int n;
+    if (words) {
+      whff::WordSink ws{words, total, 0u, 0};
+      n = whff::encode_one(pl.mag, pl.negm, pl.code, pl.planes, pl.raw, pl.raw_words,
+                           budget, has_raw, ws);
+      ws.finish();
+    } else {
+      whff::CountSink cs;
+      n = whff::encode_one(pl.mag, pl.negm, pl.code, pl.planes, pl.raw, pl.raw_words,
+                           budget, has_raw, cs);
+    }
+    if (budget) n = budget;
+    total += (uint64_t)n;
+  }
+  return (int64_t)total;
+}
+}
