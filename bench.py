@@ -1,0 +1,523 @@
+#!/usr/bin/env python
+"""WHFF paper-scale step benchmark (BASELINE.json configs[2], N=1; configs[3]
+under torchrun N>1).
+
+One step = thermal update + interpolation (T = 608^2, S = 256,000, nnz 7) and
+the x/y/z field products D_d = C_d,field S, C_d,field = 52 slits x 378 rows x
+256,000 columns per axis held as FixedRate(8) WHFZ streams in HBM (15.18 GB;
+~30.2 GFLOP per step), decoded on the fly by the fused kernel.
+
+Prints one JSON line (rank 0).  `value` is compressed GB/s over the whole job
+(payload + device index bytes of every slit stream / step time, max over
+ranks); GFLOP/s, decoded-equivalent GB/s and the per-step p50/p99 latency
+against the 50 ms firm deadline ride along.  `--impl reference` times the
+reference's own CPU path (oracle/_ref: whff.codec.decompress + mpgemv.gemv)
+on a bounded sample of the same workload with all host cores.
+"""
+
+from __future__ import annotations
+
+import argparse
+import json
+import os
+import statistics
+import subprocess
+import sys
+import tempfile
+import time
+
+ROOT = os.path.dirname(os.path.abspath(__file__))
+sys.path.insert(0, ROOT)
+
+METRIC = "fused decompress+GEMV GB/s and GFLOP/s per GPU; p99 step latency vs 50 ms"
+DEADLINE_MS = 50.0
+
+
+def parse():
+    ap = argparse.ArgumentParser()
+    ap.add_argument("--gpus", type=int, default=1)
+    ap.add_argument("--steps", type=int, default=20)
+    ap.add_argument("--warmup", type=int, default=5)
+    ap.add_argument("--impl", default="b200", choices=["b200", "reference"])
+    ap.add_argument("--mode", default="rate:8", help="rate:BPV | precision:P | accuracy:TOL")
+    ap.add_argument("--evaluation", default="exact", choices=["exact", "coefficient"])
+    ap.add_argument("--policy", default="mixed", choices=["mixed", "single", "double"])
+    ap.add_argument("--slits", type=int, default=52)
+    ap.add_argument("--rows", type=int, default=378)
+    ap.add_argument("--S", type=int, default=256000)
+    ap.add_argument("--grid", type=int, default=608)
+    ap.add_argument("--distinct", type=int, default=0,
+                    help="distinct slit contents per axis (0 = all); the rest are "
+                         "physically distinct HBM copies")
+    ap.add_argument("--vector-mode", default="broadcast", choices=["broadcast", "replicate"])
+    ap.add_argument("--no-cpu-baseline", action="store_true")
+    ap.add_argument("--cpu-sample-cols", type=int, default=8192)
+    ap.add_argument("--no-graph", action="store_true")
+    return ap.parse_args()
+
+
+def parse_mode(s):
+    from paper_1902_08018_b200 import codec
+    kind, p = s.split(":")
+    if kind == "rate":
+        return codec.FixedRate(int(p))
+    if kind == "precision":
+        return codec.FixedPrecision(int(p))
+    return codec.FixedAccuracy(float(p))
+
+
+def peaks():
+    try:
+        with open(os.path.join(ROOT, "MEASURED_PEAKS.json")) as fh:
+            return json.load(fh), "measured"
+    except Exception:
+        return {"hbm_gbs": 6650.0}, "fallback"
+
+
+class Clocks:
+    """nvidia-smi clocks/throttle sampling during the timed region."""
+    Q = ("index,clocks.sm,clocks.max.sm,power.draw,clocks_event_reasons.active,"
+         "clocks_event_reasons.hw_slowdown,clocks_event_reasons.hw_thermal_slowdown,"
+         "clocks_event_reasons.sw_thermal_slowdown,clocks_event_reasons.sw_power_cap")
+
+    def __init__(self, index):
+        self.index = index
+        self.proc = None
+        self.path = None
+
+    def start(self):
+        try:
+            fd, self.path = tempfile.mkstemp(suffix=".csv")
+            os.close(fd)
+            self.fh = open(self.path, "w")
+            self.proc = subprocess.Popen(
+                ["nvidia-smi", f"--id={self.index}", f"--query-gpu={self.Q}",
+                 "--format=csv,noheader,nounits", "-lms", "100"],
+                stdout=self.fh, stderr=subprocess.DEVNULL)
+        except Exception:
+            self.proc = None
+
+    def stop(self):
+        out = {"sm_mhz": None, "sm_max_mhz": None, "reasons": [], "samples": 0}
+        if self.proc is None:
+            return out
+        time.sleep(0.25)
+        self.proc.terminate()
+        try:
+            self.proc.wait(timeout=5)
+        except Exception:
+            self.proc.kill()
+        self.fh.close()
+        sm, mx, reasons = [], [], set()
+        names = ["hw_slowdown", "hw_thermal_slowdown", "sw_thermal_slowdown", "sw_power_cap"]
+        for line in open(self.path):
+            f = [x.strip() for x in line.split(",")]
+            if len(f) < 9:
+                continue
+            try:
+                sm.append(float(f[1]))
+                mx.append(float(f[2]))
+            except ValueError:
+                continue
+            for n, val in zip(names, f[5:9]):
+                if val.lower() == "active":
+                    reasons.add(n)
+        os.unlink(self.path)
+        if sm:
+            out = {"sm_mhz": statistics.median(sm), "sm_max_mhz": max(mx),
+                   "reasons": sorted(reasons), "samples": len(sm)}
+        return out
+
+
+# ---------------------------------------------------------------------------
+# distributed plumbing
+# ---------------------------------------------------------------------------
+
+def dist_setup(args):
+    world = int(os.environ.get("WORLD_SIZE", "1"))
+    rank = int(os.environ.get("RANK", "0"))
+    local = int(os.environ.get("LOCAL_RANK", "0"))
+    return world, rank, local
+
+
+# ---------------------------------------------------------------------------
+# workload construction
+# ---------------------------------------------------------------------------
+
+def build_field(args, world, rank):
+    import numpy as np
+    import torch
+    from paper_1902_08018_b200 import codec, synth, thermal
+    from paper_1902_08018_b200.executor import FieldStep, shard_units
+
+    K = args.slits * args.rows
+    spec = synth.Spec(grid_rows=args.grid, grid_cols=args.grid, S=args.S, K=K, M=args.rows,
+                      nnz_target=7, seed=7, n_fields=1)
+    t0 = time.time()
+    ops = synth.generate(spec)
+    dark, fps, dose = synth.heatload(spec, 1, args.slits, seed=0)
+    t_ops = time.time() - t0
+    mode = parse_mode(args.mode)
+    jobs, _ = shard_units(3, args.slits, args.rows, world, rank)
+    need = sorted({(a, s) for a, s, _, _ in jobs})
+    distinct = args.distinct if args.distinct > 0 else args.slits
+    streams = [[None] * args.slits for _ in range(3)]
+    made = {}
+    t0 = time.time()
+    for a, s in need:
+        src = s % distinct
+        if (a, src) not in made:
+            rows = synth.deformation_rows(spec, a, ops.phases[synth.AXES[a]], src * args.rows,
+                                          (src + 1) * args.rows, device="cuda")
+            made[(a, src)] = codec.compress_device(rows, mode)
+            del rows
+            streams[a][src] = made[(a, src)]
+        if streams[a][s] is None:
+            streams[a][s] = made[(a, src)].clone()
+    torch.cuda.synchronize()
+    t_enc = time.time() - t0
+    A = thermal.DeviceCSR(ops.A64())
+    P = thermal.DeviceCSR(ops.P64())
+    B = torch.from_numpy(ops.B).cuda()
+    fs = FieldStep(A, B, P, streams, args.rows, args.slits, torch.from_numpy(dark).cuda(),
+                   torch.from_numpy(fps[(0, 0)]).cuda(), dose, policy=args.policy,
+                   evaluation=args.evaluation, world=world, rank=rank,
+                   vector_mode=args.vector_mode)
+    stream_bytes = sum(ds.payload_bytes + ds.index_bytes
+                       for row in streams for ds in row if ds is not None)
+    info = {"t_ops_s": round(t_ops, 2), "t_encode_s": round(t_enc, 2),
+            "streams": sum(1 for row in streams for ds in row if ds is not None),
+            "distinct_per_axis": distinct, "stream_bytes_rank": stream_bytes,
+            "index_kind": streams[need[0][0]][need[0][1]].index_kind if need else None}
+    return fs, spec, ops, mode, streams, info
+
+
+# ---------------------------------------------------------------------------
+# CPU reference leg
+# ---------------------------------------------------------------------------
+
+def _ref_task(payload_path):
+    import numpy as np
+    sys.path.insert(0, os.path.join(ROOT, "oracle", "_ref"))
+    from whff import codec as rc
+    from whff import mpgemv as rm
+    d = np.load(payload_path, allow_pickle=True)
+    kind, p = str(d["kind"]), d["param"].item()
+    mode = {"rate": rc.FixedRate, "precision": rc.FixedPrecision, "accuracy": rc.FixedAccuracy}[kind](
+        int(p) if kind != "accuracy" else float(p))
+    s = rc.CompressedStream(mode=mode, rows=int(d["rows"]), cols=int(d["cols"]), payload=d["payload"],
+                            block_index=d["index"], total_bits=int(d["total_bits"]))
+    t0 = time.perf_counter()
+    C = rc.decompress(s)
+    y = rm.gemv(rm.GemvRequest(C, d["v"], "mixed", "sequential"))
+    return time.perf_counter() - t0, int(d["payload"].size), int(C.size), float(y.sum())
+
+
+def _port_task(payload_path):
+    import numpy as np
+    from oracle import oracle as orc
+    from types import SimpleNamespace
+    d = np.load(payload_path, allow_pickle=True)
+    kind, p = str(d["kind"]), d["param"].item()
+    s = SimpleNamespace(mode=(kind, p), rows=int(d["rows"]), cols=int(d["cols"]),
+                        payload=d["payload"], block_index=d["index"])
+    t0 = time.perf_counter()
+    C = orc.decompress(s)
+    y = orc.gemv_kernel(C, d["v"], "mixed", "sequential")
+    return time.perf_counter() - t0, int(d["payload"].size), int(C.size), float(y.sum())
+
+
+def make_cpu_samples(args, tmpdir):
+    """Bounded sample of the workload: one rows x cols chunk of a slit per
+    axis, compressed on the GPU (byte-identical to the reference encoder)."""
+    import numpy as np
+    import torch
+    from paper_1902_08018_b200 import codec, synth
+    K = args.slits * args.rows
+    spec = synth.Spec(grid_rows=args.grid, grid_cols=args.grid, S=args.S, K=K, M=args.rows,
+                      nnz_target=7, seed=7, n_fields=1)
+    mode = parse_mode(args.mode)
+    code, param = codec.mode_code(mode)
+    kind = {0: "rate", 1: "precision", 2: "accuracy"}[code]
+    rng = np.random.default_rng(0)
+    paths = []
+    for a in range(3):
+        rows = synth.deformation_rows(spec, a, 0.5 + a, 0, args.rows, device="cuda")
+        rows = rows[:, : args.cpu_sample_cols].contiguous()
+        s = codec.compress(rows, mode)
+        v = rng.random(rows.shape[1]).astype(np.float32)
+        path = os.path.join(tmpdir, f"sample{a}.npz")
+        np.savez(path, kind=kind, param=np.array(param), rows=s.rows, cols=s.cols,
+                 payload=s.payload, index=s.block_index, total_bits=s.total_bits, v=v)
+        paths.append(path)
+    torch.cuda.synchronize()
+    return paths
+
+
+def run_cpu_leg(paths, reps, warmup=0):
+    """Run the CPU path over `reps` x samples with all host cores; returns
+    (GB/s compressed, seconds, cores, kind, per-sample seconds)."""
+    import multiprocessing as mp
+    have_ref = os.path.isdir(os.path.join(ROOT, "oracle", "_ref", "whff"))
+    task = _ref_task if have_ref else _port_task
+    kind = "reference" if have_ref else "port"
+    cores = len(os.sched_getaffinity(0)) if hasattr(os, "sched_getaffinity") else os.cpu_count()
+    work = [p for _ in range(reps) for p in paths]
+    ctx = mp.get_context("fork")
+    with ctx.Pool(cores) as pool:
+        if warmup:
+            pool.map(task, paths[:1] * min(cores, warmup))
+        t0 = time.perf_counter()
+        res = pool.map(task, work, chunksize=1)
+        wall = time.perf_counter() - t0
+    nbytes = sum(r[1] for r in res)
+    per = statistics.median(r[0] for r in res)
+    return nbytes / wall / 1e9, wall, cores, kind, per, sum(r[2] for r in res)
+
+
+# ---------------------------------------------------------------------------
+# main legs
+# ---------------------------------------------------------------------------
+
+def reference_main(args, world, rank):
+    if rank != 0:
+        return 0
+    import torch
+    tmp = tempfile.mkdtemp()
+    paths = make_cpu_samples(args, tmp)
+    # each step = one pass over the 3-axis sample on all cores
+    cores = len(os.sched_getaffinity(0)) if hasattr(os, "sched_getaffinity") else os.cpu_count()
+    reps = max(1, cores // 3)
+    for _ in range(args.warmup):
+        run_cpu_leg(paths, 1)
+    times, gbs = [], []
+    total_bytes = 0
+    t_all = 0.0
+    for _ in range(args.steps):
+        v, wall, cores, kind, per, vals = run_cpu_leg(paths, reps)
+        times.append(wall)
+        t_all += wall
+        total_bytes += v * wall * 1e9
+    value = total_bytes / t_all / 1e9
+    line = {
+        "impl": "reference", "metric": METRIC, "value": round(value, 6), "unit": "GB/s",
+        "n_gpus": args.gpus, "steps": args.steps, "warmup": args.warmup,
+        "ms_per_step": round(1e3 * t_all / args.steps, 3), "higher_is_better": True,
+        "scaling": "weak", "vs_baseline": None, "dtype": "f32 products, f64 accumulate",
+        "data": "synthetic (reference smooth-C formula, model.py:252-268)",
+        "config": {"workload": "paper-scale WHFF step sample (configs[2])",
+                   "mode": args.mode, "sample": f"3 axes x {args.rows}x{args.cpu_sample_cols} slit chunk"
+                                                 f" x {reps} per step"},
+        "cpu_baseline": {"value": round(value, 6), "unit": "GB/s", "cores": cores, "kind": kind,
+                         "sample": f"reference codec.decompress + mpgemv.gemv(mixed, sequential), "
+                                   f"{3 * reps} chunks of {args.rows}x{args.cpu_sample_cols} per step"},
+        "e2e": {"value": round(value, 6), "unit": "GB/s", "h2d_bytes_per_step": 0,
+                "d2h_bytes_per_step": 0},
+    }
+    print(json.dumps(line), flush=True)
+    return 0
+
+
+def b200_main(args, world, rank, local):
+    import numpy as np
+    import torch
+    import torch.distributed as dist
+
+    torch.cuda.set_device(local)
+    group = None
+    if world > 1:
+        dist.init_process_group("nccl", device_id=torch.device("cuda", local))
+    from paper_1902_08018_b200 import _lib
+    _lib.lib()
+
+    fs, spec, ops, mode, streams, info = build_field(args, world, rank)
+    plan = fs.plan
+    cur = torch.cuda.current_stream()
+
+    use_graph = (world == 1 or args.vector_mode == "replicate") and not args.no_graph
+    if use_graph:
+        fs.capture()
+
+    def step():
+        if use_graph:
+            fs.replay()
+        else:
+            fs.step_local()
+        if world > 1:
+            dist.all_gather_into_tensor(fs.gathered, fs.local)
+
+    for _ in range(max(3, args.warmup)):
+        step()
+    torch.cuda.synchronize()
+    fs.check()
+
+    # ---- timed region: K steps, per-step events -----------------------------
+    clocks = Clocks(local)
+    ev = [torch.cuda.Event(enable_timing=True) for _ in range(args.steps + 1)]
+    if world > 1:
+        dist.barrier()
+    torch.cuda.synchronize()
+    clocks.start()
+    ev[0].record(cur)
+    for i in range(args.steps):
+        step()
+        ev[i + 1].record(cur)
+    torch.cuda.synchronize()
+    if world > 1:
+        dist.barrier()
+    clk = clocks.stop()
+    step_ms = [ev[i].elapsed_time(ev[i + 1]) for i in range(args.steps)]
+    total_ms = ev[0].elapsed_time(ev[-1])
+    fs.check()
+
+    # ---- dominant kernel alone (fused decode+GEMV plan launch) ---------------
+    k0, k1 = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
+    nk = max(3, args.steps // 2)
+    plan.launch(fs.status)
+    torch.cuda.synchronize()
+    k0.record(cur)
+    for _ in range(nk):
+        plan.launch(fs.status)
+    k1.record(cur)
+    torch.cuda.synchronize()
+    kernel_ms = k0.elapsed_time(k1) / nk
+
+    # ---- e2e through the public API with host buffers ------------------------
+    T = spec.T
+    u_host = torch.from_numpy((ops.B * 0 + 1e-3).astype(np.float32)).pin_memory()
+    out_rows = fs.gathered.numel() if world > 1 else fs.local.numel()
+    d_host = torch.empty(out_rows, dtype=torch.float32).pin_memory()
+    from paper_1902_08018_b200.thermal import csr_matvec
+
+    def e2e_step():
+        fs.u.copy_(u_host, non_blocking=True)
+        fs.status.fill_(-1)
+        if world == 1 or args.vector_mode == "replicate" or rank == 0:
+            csr_matvec(fs.A, fs.T, fs.B, fs.u, out=fs.T_next)
+            csr_matvec(fs.P, fs.T_next, out=fs.S)
+            fs.T.copy_(fs.T_next)
+        if world > 1 and args.vector_mode == "broadcast":
+            dist.broadcast(fs.S, src=0)
+        fs.products()
+        if world > 1:
+            dist.all_gather_into_tensor(fs.gathered, fs.local)
+            d_host.copy_(fs.gathered, non_blocking=True)
+        else:
+            d_host.copy_(fs.local, non_blocking=True)
+        cur.synchronize()
+
+    for _ in range(2):
+        e2e_step()
+    e0, e1 = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
+    if world > 1:
+        dist.barrier()
+    t0 = time.perf_counter()
+    e0.record(cur)
+    for _ in range(args.steps):
+        e2e_step()
+    e1.record(cur)
+    torch.cuda.synchronize()
+    e2e_ms = max(e0.elapsed_time(e1), 1e3 * (time.perf_counter() - t0)) / args.steps
+
+    # ---- reduce over ranks -------------------------------------------------
+    stats = torch.tensor([total_ms, e2e_ms, kernel_ms, float(info["stream_bytes_rank"]),
+                          float(plan.bytes_read + plan.bytes_written) if plan else 0.0],
+                         dtype=torch.float64, device="cuda")
+    per_step = torch.tensor(step_ms, dtype=torch.float64, device="cuda")
+    if world > 1:
+        mx = stats.clone()
+        dist.all_reduce(mx, op=dist.ReduceOp.MAX)
+        sm = stats.clone()
+        dist.all_reduce(sm, op=dist.ReduceOp.SUM)
+        dist.all_reduce(per_step, op=dist.ReduceOp.MAX)
+        total_ms, e2e_ms, kernel_ms = mx[0].item(), mx[1].item(), mx[2].item()
+        job_bytes, kernel_bytes = sm[3].item(), mx[4].item()
+    else:
+        job_bytes, kernel_bytes = float(info["stream_bytes_rank"]), stats[4].item()
+    step_ms = per_step.cpu().tolist()
+
+    # ---- CPU baseline beside it (rank 0, N=1) --------------------------------
+    cpu = None
+    if rank == 0 and world == 1 and not args.no_cpu_baseline:
+        tmp = tempfile.mkdtemp()
+        paths = make_cpu_samples(args, tmp)
+        cores = len(os.sched_getaffinity(0)) if hasattr(os, "sched_getaffinity") else os.cpu_count()
+        v, wall, cores, kind, per, _ = run_cpu_leg(paths, max(1, cores // 3))
+        cpu = {"value": round(v, 6), "unit": "GB/s", "cores": cores, "kind": kind,
+               "sample": f"{3 * max(1, cores // 3)} chunks of {args.rows}x{args.cpu_sample_cols} "
+                         f"({args.mode}), reference codec.decompress + mpgemv.gemv(mixed, sequential); "
+                         f"{wall:.1f}s wall"}
+
+    if rank != 0:
+        if world > 1:
+            dist.destroy_process_group()
+        return 0
+
+    pk, pk_kind = peaks()
+    hbm = float(pk.get("hbm_gbs", 6650.0))
+    K = args.slits * args.rows
+    flops = 3 * K * (2 * args.S - 1)
+    decoded_bytes = 3 * K * args.S * 4
+    steps_s = total_ms / 1e3
+    value = job_bytes * args.steps / steps_s / 1e9
+    achieved = kernel_bytes / (kernel_ms / 1e3) / 1e9
+    traffic = None
+    try:
+        with open(os.path.join(ROOT, "profiles", "ncu_traffic.json")) as fh:
+            tj = json.load(fh)
+            if tj.get("mode") == args.mode and tj.get("evaluation") == args.evaluation:
+                traffic = tj.get("dram_bytes_per_launch")
+    except Exception:
+        pass
+    p50 = statistics.median(step_ms)
+    p99 = sorted(step_ms)[min(len(step_ms) - 1, int(0.99 * len(step_ms)))]
+    launches_per_step = 4 + (1 if args.evaluation == "coefficient" else 0)
+    line = {
+        "metric": METRIC, "value": round(value, 3), "unit": "GB/s",
+        "n_gpus": world, "steps": args.steps, "warmup": args.warmup,
+        "ms_per_step": round(total_ms / args.steps, 4), "higher_is_better": True,
+        "scaling": "strong", "vs_baseline": None,
+        "dtype": "f32 products, f64 accumulate" if args.policy == "mixed" else args.policy,
+        "data": "synthetic (reference smooth-C formula model.py:252-268, seed 7); "
+                f"{info['distinct_per_axis']} distinct slits/axis",
+        "config": {"workload": "paper-scale WHFF step (configs[2]): thermal T=608^2 nnz7 + "
+                               f"3 axes x {args.slits} slits x {args.rows}x{args.S}",
+                   "mode": args.mode, "evaluation": args.evaluation, "policy": args.policy,
+                   "parallelism": f"row-shard{world}" if world > 1 else "single",
+                   "vector_mode": args.vector_mode if world > 1 else None,
+                   "l2": "inputs (compressed field) far larger than L2; no flush needed",
+                   "cuda_graph": use_graph, "index_kind": info["index_kind"]},
+        "gflops": round(flops * args.steps / steps_s / 1e9, 2),
+        "decoded_gbs": round(decoded_bytes * args.steps / steps_s / 1e9, 2),
+        "per_gpu_gbs": round(value / world, 3),
+        "latency_ms": {"p50": round(p50, 4), "p99": round(p99, 4), "max": round(max(step_ms), 4),
+                       "deadline": DEADLINE_MS, "deadline_met": max(step_ms) <= DEADLINE_MS},
+        "e2e": {"value": round(job_bytes / (e2e_ms / 1e3) / 1e9, 3), "unit": "GB/s",
+                "ms_per_step": round(e2e_ms, 4), "h2d_bytes_per_step": T * 4,
+                "d2h_bytes_per_step": out_rows * 4},
+        "gpu_launches": launches_per_step * args.steps,
+        "roofline": {"bound": "hbm", "kernel": "k_decode_gemv", "achieved": round(achieved, 2),
+                     "peak": hbm, "peak_kind": f"{pk_kind} hbm_gbs (burst copy)", "unit": "GB/s",
+                     "frac": round(achieved / hbm, 4), "traffic": traffic,
+                     "bytes_per_launch": int(kernel_bytes), "kernel_ms": round(kernel_ms, 4),
+                     "share_of_step": round(kernel_ms / (total_ms / args.steps), 3)},
+        "cpu_baseline": cpu,
+        "clocks": clk,
+        "setup": info,
+    }
+    print(json.dumps(line), flush=True)
+    if world > 1:
+        dist.destroy_process_group()
+    return 0
+
+
+def main():
+    args = parse()
+    world, rank, local = dist_setup(args)
+    if args.impl == "reference":
+        return reference_main(args, world, rank)
+    return b200_main(args, world, rank, local)
+
+
+if __name__ == "__main__":
+    sys.exit(main())

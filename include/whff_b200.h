@@ -120,6 +120,8 @@ whff_status_t whff_dstream_create_segments(int device, const uint8_t* payload_ho
                                            int planes_limit, int has_raw_flag,
                                            whff_dstream_t* out);
 whff_status_t whff_dstream_destroy(whff_dstream_t s);
+/* Physically distinct device copy of a stream (same device).  Synchronous. */
+whff_status_t whff_dstream_clone(whff_dstream_t s, whff_dstream_t* out);
 whff_status_t whff_dstream_get_info(whff_dstream_t s, whff_dstream_info_t* info);
 /* Copy payload (payload_bytes) and u64 block bit offsets (n_blocks) back to
  * the host, e.g. for codec.py:388-402 save_stream.  Synchronous.           */

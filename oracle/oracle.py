@@ -61,6 +61,8 @@ def lib():
         L.orc_csr_matvec_f32out.argtypes = [p, p, p, i64, p, p]
         L.orc_csr_matvec_f32out.restype = None
         L.orc_num_threads.restype = ci
+        L.orc_encode_blocks.argtypes = [p, p, p, p, p, p, i64, ci, ci, p, p]
+        L.orc_encode_blocks.restype = i64
         _lib = L
     return _lib
 
@@ -182,6 +184,26 @@ def compress(array, mode):
     assert total2 == total
     return SimpleNamespace(mode=mode, rows=rows, cols=cols, payload=payload,
                            block_index=offsets, total_bits=int(total), block_size=4)
+
+
+def encode_blocks(mag, neg, emax_code, planes, raw_mask, raw_words, n_planes, budget_bits,
+                  has_raw_flag):
+    """K:228-283 -> (payload uint8, offsets uint64, total_bits)."""
+    assert int(n_planes) == N_PLANES
+    mag = np.ascontiguousarray(mag, np.uint32)
+    neg = np.ascontiguousarray(neg, np.uint8)
+    emax = np.ascontiguousarray(emax_code, np.uint16)
+    planes = np.ascontiguousarray(planes, np.uint8)
+    raw_mask = np.ascontiguousarray(raw_mask, np.uint8)
+    raw_words = np.ascontiguousarray(raw_words, np.uint32)
+    nb = emax.size
+    offsets = np.zeros(nb, np.uint64)
+    args = [_ptr(mag), _ptr(neg), _ptr(emax), _ptr(planes), _ptr(raw_mask), _ptr(raw_words), nb,
+            int(budget_bits), int(bool(has_raw_flag)), _ptr(offsets)]
+    total = lib().orc_encode_blocks(*args, None)
+    payload = np.zeros((total + 7) // 8, np.uint8)
+    lib().orc_encode_blocks(*args, _ptr(payload))
+    return payload, offsets, int(total)
 
 
 # ---------------------------------------------------------------------------

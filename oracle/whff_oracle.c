@@ -663,3 +663,29 @@ void orc_csr_matvec_f32out(const int64_t* indptr, const int32_t* indices,
         y[i] = (float)acc;
     }
 }
+
+/* K:228-283 encode_blocks from per-block arrays.  Two calls: payload NULL
+ * returns total bits and fills offsets; then emit into a zeroed payload.   */
+int64_t orc_encode_blocks(const uint32_t* mag, const uint8_t* neg, const uint16_t* emax,
+                          const uint8_t* planes, const uint8_t* raw_mask,
+                          const uint32_t* raw_words, int64_t nb, int budget,
+                          int has_raw_flag, uint64_t* offsets, uint8_t* payload) {
+    uint8_t* tmp = (uint8_t*)calloc(ORC_MAX_BLOCK_BITS + (budget > 0 ? budget : 0) + 64, 1);
+    uint64_t total = 0;
+    for (int64_t b = 0; b < nb; b++) {
+        int64_t magl[16];
+        for (int i = 0; i < 16; i++) magl[i] = mag[16 * b + i];
+        offsets[b] = total;
+        memset(tmp, 0, ORC_MAX_BLOCK_BITS + (budget > 0 ? budget : 0) + 64);
+        int n = encode_one(magl, neg + 16 * b, emax[b], planes[b],
+                           has_raw_flag ? raw_mask[b] : 0, raw_words + 16 * b,
+                           ORC_N_PLANES, budget, has_raw_flag, tmp);
+        if (budget) n = budget;
+        if (payload)
+            for (int i = 0; i < n; i++)
+                if (tmp[i]) payload[(total + i) >> 3] |= (uint8_t)(0x80u >> ((total + i) & 7));
+        total += n;
+    }
+    free(tmp);
+    return (int64_t)total;
+}

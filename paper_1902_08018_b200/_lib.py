@@ -45,6 +45,7 @@ _SIG = {
     "whff_dstream_create": ([_I, _I, ctypes.c_double, _U64, _U64, _P, _U64, _P, _U64, _P], _I),
     "whff_dstream_create_segments": ([_I, _P, _U64, _P, _P, _U64, _I, _I, _P], _I),
     "whff_dstream_destroy": ([_P], _I),
+    "whff_dstream_clone": ([_P, _P], _I),
     "whff_dstream_get_info": ([_P, _P], _I),
     "whff_dstream_download": ([_P, _P, _P], _I),
     "whff_compress": ([_P, _U64, _U64, _U64, _I, ctypes.c_double, _P, _P], _I),

@@ -195,6 +195,12 @@ class DeviceStream:
                   _lib.ptr(payload), payload.size, _lib.ptr(index), index.size, ctypes.byref(h))
         return cls(h, stream.mode, total_bits=int(stream.total_bits))
 
+    def clone(self):
+        """A physically distinct HBM copy (whff_dstream_clone)."""
+        h = ctypes.c_void_p()
+        _lib.call("whff_dstream_clone", self._h, ctypes.byref(h))
+        return DeviceStream(h, self.mode, total_bits=self.total_bits)
+
     def to_host(self):
         payload = np.empty(self.payload_bytes, dtype=np.uint8)
         index = np.empty(self.n_blocks, dtype=np.uint64)

@@ -145,10 +145,10 @@ __global__ void __launch_bounds__(128) k_decode_blocks(StreamView s, uint64_t fi
   uint64_t start;
   int len;
   block_extent(s, b, start, len);
-  BitWindow bw;
-  window_at(bw, s.words, start);
+  BitWin bw;
+  win_at(bw, s.words, start, len);
   Decoded d;
-  decode_block<HAS_RAW, true>(bw, len, planes_limit, d);
+  decode_block<HAS_RAW, true>(bw, planes_limit, d, __activemask());
   emax[i] = (uint16_t)d.emax;
   raw[i] = (uint8_t)d.raw;
   consumed[i] = (uint64_t)d.consumed;
@@ -171,10 +171,10 @@ __global__ void __launch_bounds__(128) k_decode_block_words(StreamView s, uint64
   uint64_t start;
   int len;
   block_extent(s, first + i, start, len);
-  BitWindow bw;
-  window_at(bw, s.words, start);
+  BitWin bw;
+  win_at(bw, s.words, start, len);
   Decoded d;
-  decode_block<HAS_RAW, true>(bw, len, s.planes_limit, d);
+  decode_block<HAS_RAW, true>(bw, s.planes_limit, d, __activemask());
   float x[16];
   reconstruct_words(d, x);
 #pragma unroll
@@ -192,10 +192,10 @@ __global__ void __launch_bounds__(128) k_decode_words(StreamView s, float* out, 
   uint64_t start;
   int len;
   block_extent(s, b, start, len);
-  BitWindow bw;
-  window_at(bw, s.words, start);
+  BitWin bw;
+  win_at(bw, s.words, start, len);
   Decoded d;
-  decode_block<HAS_RAW, true>(bw, len, s.planes_limit, d);
+  decode_block<HAS_RAW, true>(bw, s.planes_limit, d, __activemask());
   float x[16];
   reconstruct_words(d, x);
   const uint64_t r0 = (b / s.bc) * 4, c0 = (b % s.bc) * 4;
@@ -319,24 +319,27 @@ template <> struct VarTraits<2> { static constexpr bool kRefill = true, kRaw = f
 // 3: indexed with raw flag (fixed accuracy)
 template <> struct VarTraits<3> { static constexpr bool kRefill = true, kRaw = true, kIndexed = true; };
 
+constexpr int kGemvWarps = 8;
+
 template <int VAR, int EVAL>
 __global__ void __launch_bounds__(256) k_decode_gemv(JobTable T, int policy,
                                                      unsigned long long* status) {
   using TR = VarTraits<VAR>;
-  const uint64_t gw = (blockIdx.x * (uint64_t)blockDim.x + threadIdx.x) >> 5;
-  if (gw >= T.total_warps) return;
+  // one CTA per (job, block-row); its 8 warps split the row's 32-block groups
+  const uint64_t gr = blockIdx.x;
+  if (gr >= T.total_warps) return;
   const int lane = threadIdx.x & 31;
-
-  uint64_t first_warp = 0;
+  const int warp = threadIdx.x >> 5;
+  uint64_t first_row = 0;
   int jidx = -1;
   if (T.jobs != nullptr) {
     int lo = 0, hi = T.n - 1;
     while (lo < hi) {
       const int mid = (lo + hi + 1) >> 1;
-      if (T.prefix[mid] <= gw) lo = mid; else hi = mid - 1;
+      if (T.prefix[mid] <= gr) lo = mid; else hi = mid - 1;
     }
     jidx = lo;
-    first_warp = T.prefix[lo];
+    first_row = T.prefix[lo];
   }
   const StreamView s = jidx < 0 ? T.single.s : T.jobs[jidx].s;
   const float* __restrict__ v = jidx < 0 ? T.single.v : T.jobs[jidx].v;
@@ -345,7 +348,7 @@ __global__ void __launch_bounds__(256) k_decode_gemv(JobTable T, int policy,
   const uint64_t row_begin = jidx < 0 ? T.single.row_begin : T.jobs[jidx].row_begin;
   const uint64_t row_end = jidx < 0 ? T.single.row_end : T.jobs[jidx].row_end;
   const uint64_t br0 = jidx < 0 ? T.single.br0 : T.jobs[jidx].br0;
-  const uint64_t brow = br0 + (gw - first_warp);
+  const uint64_t brow = br0 + (gr - first_row);
   const uint64_t bc = s.bc;
   const bool v_aligned = ((reinterpret_cast<uintptr_t>(v) & 15u) == 0);
   const uint32_t last_colmask = (s.cols & 3) ? ((1u << (s.cols & 3)) - 1u) : 0xFu;
@@ -361,28 +364,30 @@ __global__ void __launch_bounds__(256) k_decode_gemv(JobTable T, int policy,
   const uint64_t row_block0 = brow * bc;
   const uint4* __restrict__ seg128 = reinterpret_cast<const uint4*>(s.words);
   uint4 nxt = make_uint4(0, 0, 0, 0);
-  if (VAR == 0 && (uint64_t)lane < bc) nxt = ldg(seg128 + row_block0 + lane);
+  if (VAR == 0) {
+    const uint64_t bcol0 = (uint64_t)warp * 32 + lane;
+    if (bcol0 < bc) nxt = ldg(seg128 + row_block0 + bcol0);
+  }
 
-  for (uint64_t g = 0; g < s.gpr; ++g) {
+  for (uint64_t g = warp; g < s.gpr; g += kGemvWarps) {
     const uint64_t bcol = g * 32 + lane;
     const bool active = bcol < bc;
     const uint64_t b = row_block0 + bcol;
-    BitWindow bw;
-    int len = 0;
+    BitWin bw;
+    Decoded d;
     if (VAR == 0) {
       const uint4 q = nxt;
-      if (bcol + 32 < bc) nxt = ldg(seg128 + b + 32);   // prefetch next group
-      bw.w0 = bswap32(q.x); bw.w1 = bswap32(q.y); bw.w2 = bswap32(q.z); bw.w3 = bswap32(q.w);
-      bw.off = 0;
-      bw.src = nullptr;
-      len = clamp_len(b * 128ull, 128ull, s.payload_bits);
-    } else if (!TR::kIndexed) {
-      const uint64_t start = b * (uint64_t)s.seg_bits;
-      len = active ? clamp_len(start, s.seg_bits, s.payload_bits) : 0;
-      if (active) window_at(bw, s.words, start);
+      const uint64_t bn = bcol + 32 * kGemvWarps;
+      if (bn < bc) nxt = ldg(seg128 + row_block0 + bn);   // prefetch this warp's next group
+      win_128(bw, q.x, q.y, q.z, q.w, active ? clamp_len(b * 128ull, 128ull, s.payload_bits) : 0);
+      decode_block<false, false>(bw, pl, d, 0xFFFFFFFFu);
     } else {
       uint64_t start = 0;
-      if (s.kind == WHFF_INDEX_COMPACT) {
+      int len = 0;
+      if (!TR::kIndexed) {
+        start = b * (uint64_t)s.seg_bits;
+        if (active) len = clamp_len(start, s.seg_bits, s.payload_bits);
+      } else if (s.kind == WHFF_INDEX_COMPACT) {
         const uint32_t l = active ? (uint32_t)s.lens[b] : 0u;
         uint32_t incl = l;
 #pragma unroll
@@ -391,17 +396,26 @@ __global__ void __launch_bounds__(256) k_decode_gemv(JobTable T, int policy,
           if (lane >= o) incl += t;
         }
         start = s.base[brow * s.gpr + g] + (incl - l);
-        len = active ? clamp_len(start, l, s.payload_bits) : 0;
+        if (active) len = clamp_len(start, l, s.payload_bits);
       } else if (active) {
         start = s.starts[b];
         len = clamp_len(start, s.lens[b], s.payload_bits);
       }
-      if (active) window_at(bw, s.words, start);
+      if (active) {
+        win_at(bw, s.words, start, len);
+      } else {
+        bw.w0 = bw.w1 = bw.w2 = bw.w3 = 0u;
+        bw.pos = 0;
+        bw.len = 0;
+        bw.avail = 128;
+        bw.src = s.words;
+      }
+      if (__any_sync(0xFFFFFFFFu, active && !fits_no_refill(start, len)))
+        decode_block<TR::kRaw, true>(bw, pl, d, 0xFFFFFFFFu);
+      else
+        decode_block<TR::kRaw, false>(bw, pl, d, 0xFFFFFFFFu);
     }
     if (!active) continue;
-
-    Decoded d;
-    decode_block<TR::kRaw, TR::kRefill>(bw, len, pl, d);
     const uint32_t colmask = (bcol + 1 == bc) ? last_colmask : 0xFu;
 
     if (EVAL == WHFF_EVAL_EXACT) {
@@ -410,42 +424,26 @@ __global__ void __launch_bounds__(256) k_decode_gemv(JobTable T, int policy,
       reconstruct_words(d, x);
       acc_exact(A, policy, x, v4, colmask);
     } else {
-      if (d.raw || d.emax == 0) {
-        if (d.raw) {
-          const float4 v4 = load_v4(v, bcol, s.cols, v_aligned);
-          float x[16];
-          reconstruct_words(d, x);
-          Acc R;
+      const int k = (int)d.emax - kEmaxBias - kQuantBits;
+      if (!d.raw && d.emax != 0 && k >= -126 && k <= 100) {
+        acc_coeff(A, policy, d, ldg(U + bcol), k);
+      } else if (d.raw || d.emax != 0) {   // raw escape / extreme scale: exact spatial path
+        const float4 v4 = load_v4(v, bcol, s.cols, v_aligned);
+        float x[16];
+        reconstruct_words(d, x);
+        Acc R;
 #pragma unroll
-          for (int i = 0; i < 4; ++i) { R.d[i] = accR[i]; R.f[i] = accRf[i]; }
-          R.probe = A.probe;
-          acc_exact(R, policy, x, v4, colmask);
+        for (int i = 0; i < 4; ++i) { R.d[i] = accR[i]; R.f[i] = accRf[i]; }
+        R.probe = A.probe;
+        acc_exact(R, policy, x, v4, colmask);
 #pragma unroll
-          for (int i = 0; i < 4; ++i) { accR[i] = R.d[i]; accRf[i] = R.f[i]; }
-          A.probe = R.probe;
-        }
-      } else {
-        const int k = (int)d.emax - kEmaxBias - kQuantBits;
-        if (k >= -126 && k <= 100) {
-          acc_coeff(A, policy, d, ldg(U + bcol), k);
-        } else {  // out of the normal fp32 scale range: exact spatial path
-          const float4 v4 = load_v4(v, bcol, s.cols, v_aligned);
-          float x[16];
-          reconstruct_words(d, x);
-          Acc R;
-#pragma unroll
-          for (int i = 0; i < 4; ++i) { R.d[i] = accR[i]; R.f[i] = accRf[i]; }
-          R.probe = A.probe;
-          acc_exact(R, policy, x, v4, colmask);
-#pragma unroll
-          for (int i = 0; i < 4; ++i) { accR[i] = R.d[i]; accRf[i] = R.f[i]; }
-          A.probe = R.probe;
-        }
+        for (int i = 0; i < 4; ++i) { accR[i] = R.d[i]; accRf[i] = R.f[i]; }
+        A.probe = R.probe;
       }
     }
   }
 
-  // fixed xor butterfly over the warp (deterministic)
+  // fixed xor butterfly over the warp, then the 8 warps in order (deterministic)
 #pragma unroll
   for (int o = 16; o > 0; o >>= 1) {
 #pragma unroll
@@ -459,31 +457,56 @@ __global__ void __launch_bounds__(256) k_decode_gemv(JobTable T, int policy,
     }
     A.probe = __fadd_rn(A.probe, __shfl_xor_sync(0xFFFFFFFFu, A.probe, o));
   }
-  if (lane < 4) {
-    const int i = lane;
+  __shared__ double sd[kGemvWarps][4], sR[kGemvWarps][4];
+  __shared__ float sf[kGemvWarps][4], sRf[kGemvWarps][4], sp[kGemvWarps];
+  if (lane == 0) {
+#pragma unroll
+    for (int i = 0; i < 4; ++i) {
+      sd[warp][i] = A.d[i];
+      sf[warp][i] = A.f[i];
+      sR[warp][i] = accR[i];
+      sRf[warp][i] = accRf[i];
+    }
+    sp[warp] = A.probe;
+  }
+  __syncthreads();
+  if (threadIdx.x < 4) {
+    const int i = threadIdx.x;
+    double td[4] = {0.0, 0.0, 0.0, 0.0}, tR = 0.0;
+    float tf[4] = {0.0f, 0.0f, 0.0f, 0.0f}, tRf = 0.0f, probe = 0.0f;
+    for (int w = 0; w < kGemvWarps; ++w) {
+#pragma unroll
+      for (int a = 0; a < 4; ++a) {
+        td[a] = __dadd_rn(td[a], sd[w][a]);
+        tf[a] = __fadd_rn(tf[a], sf[w][a]);
+      }
+      tR = __dadd_rn(tR, sR[w][i]);
+      tRf = __fadd_rn(tRf, sRf[w][i]);
+      probe = __fadd_rn(probe, sp[w]);
+    }
     const uint64_t r = brow * 4 + i;
     if (r >= row_begin && r < row_end && r < s.rows) {
       float out;
       bool bad;
       if (EVAL == WHFF_EVAL_EXACT) {
         if (policy == WHFF_POLICY_SINGLE) {
-          out = A.f[i];
-          bad = !isfinite(A.probe);
+          out = tf[i];
+          bad = !isfinite(probe);
         } else {
-          out = __double2float_rn(A.d[i]);
-          bad = !isfinite(A.d[i]);
+          out = __double2float_rn(td[i]);
+          bad = !isfinite(td[i]);
         }
       } else {
         if (policy == WHFF_POLICY_SINGLE) {
-          float t = accRf[i];
+          float t = tRf;
 #pragma unroll
-          for (int a = 0; a < 4; ++a) t = __fmaf_rn(c_G[i][a], A.f[a], t);
+          for (int a = 0; a < 4; ++a) t = __fmaf_rn(c_G[i][a], tf[a], t);
           out = t;
-          bad = !isfinite(A.probe);
+          bad = !isfinite(probe);
         } else {
-          double t = accR[i];
+          double t = tR;
 #pragma unroll
-          for (int a = 0; a < 4; ++a) t = __fma_rn((double)c_G[i][a], A.d[a], t);
+          for (int a = 0; a < 4; ++a) t = __fma_rn((double)c_G[i][a], td[a], t);
           out = __double2float_rn(t);
           bad = !isfinite(t);
         }
@@ -694,7 +717,7 @@ __global__ void k_encode_emit(const float* a, uint64_t lda, uint64_t rows, uint6
   BlockPlan pl;
   plan_block(a, (int64_t)lda, (int64_t)rows, (int64_t)cols, (int64_t)b, (int64_t)bc, mode, param, pl);
   const int budget = mode == WHFF_MODE_RATE ? (int)param * 16 : 0;
-  WordSink ws{words, offsets[b], 0u, 0};
+  WordSink ws{words, offsets[b], 0u, 0, budget ? budget : 0x7FFFFFFF};
   encode_one(pl.mag, pl.negm, pl.code, pl.planes, pl.raw, pl.raw_words, budget,
              mode == WHFF_MODE_ACCURACY, ws);
   ws.finish();
@@ -744,7 +767,7 @@ __global__ void k_encblocks_emit(EncArrays E, uint64_t nb, int budget, int has_r
   int planes;
   bool raw;
   load_enc(E, b, has_raw, mag, negm, code, planes, raw, rw);
-  WordSink ws{words, offsets[b], 0u, 0};
+  WordSink ws{words, offsets[b], 0u, 0, budget ? budget : 0x7FFFFFFF};
   encode_one(mag, negm, code, planes, raw, rw, budget, has_raw != 0, ws);
   ws.finish();
 }
@@ -971,6 +994,34 @@ whff_status_t whff_dstream_create_segments(int device, const uint8_t* payload, u
   if (e != cudaSuccess) { free_stream(s); return cuda_fail(e, "segment stream upload"); }
   s->index_bytes = nb * 10;
   *out = s;
+  return WHFF_OK;
+}
+
+whff_status_t whff_dstream_clone(whff_dstream_t s, whff_dstream_t* out) {
+  if (!s || !out) return fail(WHFF_ERR_ARGUMENT, "null argument");
+  *out = nullptr;
+  DeviceGuard g(s->device);
+  whff_dstream* c = new whff_dstream(*s);
+  c->d_payload = nullptr;
+  c->d_base = nullptr;
+  c->d_lens = nullptr;
+  c->d_starts = nullptr;
+  cudaError_t e = cudaMalloc(&c->d_payload, s->payload_alloc);
+  if (e == cudaSuccess) e = cudaMemcpy(c->d_payload, s->d_payload, s->payload_alloc, cudaMemcpyDeviceToDevice);
+  if (e == cudaSuccess && s->d_base) {
+    e = cudaMalloc(&c->d_base, s->br * s->gpr * 8);
+    if (e == cudaSuccess) e = cudaMemcpy(c->d_base, s->d_base, s->br * s->gpr * 8, cudaMemcpyDeviceToDevice);
+  }
+  if (e == cudaSuccess && s->d_lens) {
+    e = cudaMalloc(&c->d_lens, s->nb * 2);
+    if (e == cudaSuccess) e = cudaMemcpy(c->d_lens, s->d_lens, s->nb * 2, cudaMemcpyDeviceToDevice);
+  }
+  if (e == cudaSuccess && s->d_starts) {
+    e = cudaMalloc(&c->d_starts, s->nb * 8);
+    if (e == cudaSuccess) e = cudaMemcpy(c->d_starts, s->d_starts, s->nb * 8, cudaMemcpyDeviceToDevice);
+  }
+  if (e != cudaSuccess) { free_stream(c); return cuda_fail(e, "clone"); }
+  *out = c;
   return WHFF_OK;
 }
 
@@ -1227,8 +1278,8 @@ static int variant_of(const whff_dstream* s) {
 template <int EVAL>
 static whff_status_t launch_gemv_var(int var, const JobTable& T, int policy,
                                      unsigned long long* status, cudaStream_t cs) {
-  const unsigned threads = 256;
-  const unsigned blocks = grid_for(T.total_warps * 32, threads);
+  const unsigned threads = 32 * kGemvWarps;
+  const unsigned blocks = (unsigned)T.total_warps;   // one CTA per block-row
   if (blocks == 0) return WHFF_OK;
   switch (var) {
     case 0: k_decode_gemv<0, EVAL><<<blocks, threads, 0, cs>>>(T, policy, status); break;
@@ -1263,11 +1314,12 @@ static whff_status_t check_policy_eval(int policy, int eval) {
 extern "C" whff_status_t whff_decode_gemv(whff_dstream_t s, const float* v, float* y, int policy, int eval,
                                uint64_t row_begin, uint64_t row_end, void* ws, size_t ws_bytes,
                                uint64_t* status, whff_stream_t stream) {
-  if (!s || !v || !y || !status) return fail(WHFF_ERR_ARGUMENT, "null argument");
+  if (!s) return fail(WHFF_ERR_ARGUMENT, "null stream");
   whff_status_t st = check_policy_eval(policy, eval);
   if (st != WHFF_OK) return st;
   if (row_begin > row_end || row_end > s->rows) return fail(WHFF_ERR_DIMENSION, "bad row range");
   if (row_begin == row_end) return WHFF_OK;
+  if (!v || !y || !status) return fail(WHFF_ERR_ARGUMENT, "null argument");
   cudaStream_t cs = (cudaStream_t)stream;
   JobTable T;
   T.jobs = nullptr;

@@ -104,6 +104,10 @@ WHFF_HD uint32_t byte_perm(uint32_t a, uint32_t b, uint32_t s) {
   return r;
 #endif
 }
+#if !defined(__CUDA_ARCH__)
+inline bool __all_sync(unsigned, bool v) { return v; }   // host check: one lane
+#endif
+
 template <typename T>
 WHFF_HD T ldg(const T* p) {
 #if defined(__CUDA_ARCH__)
@@ -114,42 +118,97 @@ WHFF_HD T ldg(const T* p) {
 }
 
 // ---------------------------------------------------------------------------
-// Bit window over a big-endian (np.packbits, MSB-first) bit stream.
-// w0:w1 always hold the next >= 32 bits starting at bit `off` of w0.
+// 128-bit shift-register bit window over a big-endian (np.packbits,
+// MSB-first) bit stream.  w0 holds the next 32 bits; advancing shifts the
+// whole register left (four clamped funnel shifts, no compares).  Bits at
+// segment positions >= len read as zero: parsing a zero-extended segment
+// yields exactly the reference's output (a read past the limit ends the
+// block in K:286-368, and zeros never set a magnitude bit, never raise a
+// group flag and never form a hit), except for a hit whose sign bit lies past
+// the limit, which decode_block handles explicitly (K:353-354).
 // ---------------------------------------------------------------------------
-struct BitWindow {
-  uint32_t w0, w1, w2, w3;
-  uint32_t off;
-  const uint32_t* src;  // next little-endian payload word (REFILL)
-};
-
-// Window at absolute bit offset `bit` of a payload viewed as LE uint32 words.
-// The payload allocation must be padded with >= 32 readable bytes.
-WHFF_HD void window_at(BitWindow& b, const uint32_t* words, uint64_t bit) {
-  const uint32_t* p = words + (bit >> 5);
-  b.w0 = bswap32(ldg(p));
-  b.w1 = bswap32(ldg(p + 1));
-  b.w2 = bswap32(ldg(p + 2));
-  b.w3 = bswap32(ldg(p + 3));
-  b.off = (uint32_t)(bit & 31);
-  b.src = p + 4;
+WHFF_HD uint32_t fsl(uint32_t hi, uint32_t lo, uint32_t s) {  // s in [0, 32]
+#if defined(__CUDA_ARCH__)
+  return __funnelshift_lc(lo, hi, s);
+#else
+  return s >= 32 ? lo : (s ? (hi << s) | (lo >> (32 - s)) : hi);
+#endif
+}
+WHFF_HD uint32_t top_mask(int nbits) {  // top nbits set, nbits in [0, 32]
+  return nbits <= 0 ? 0u : (nbits >= 32 ? 0xFFFFFFFFu : ~(0xFFFFFFFFu >> nbits));
 }
 
-WHFF_HD uint32_t peek32(const BitWindow& b) { return funnel_hi(b.w0, b.w1, b.off); }
+struct BitWin {
+  uint32_t w0, w1, w2, w3;
+  int pos;              // segment bits consumed
+  int len;              // segment length (bits beyond read as zero)
+  int avail;            // REFILL: valid bits held in w0..w3
+  const uint32_t* src;  // REFILL: next little-endian payload word
+};
+
+// Window at absolute bit `bit` of a payload viewed as LE uint32 words (the
+// allocation is padded with >= 32 readable bytes).  The register holds the
+// 128 - (bit & 31) bits up to the next word boundary; decode_block<.., false>
+// is therefore exact only when (bit & 31) + len <= 128 (see fits_no_refill).
+WHFF_HD void win_at(BitWin& b, const uint32_t* words, uint64_t bit, int len) {
+  const uint32_t* p = words + (bit >> 5);
+  const uint32_t off = (uint32_t)(bit & 31);
+  const uint32_t a0 = bswap32(ldg(p)), a1 = bswap32(ldg(p + 1)), a2 = bswap32(ldg(p + 2)),
+                 a3 = bswap32(ldg(p + 3));
+  b.w0 = fsl(a0, a1, off);
+  b.w1 = fsl(a1, a2, off);
+  b.w2 = fsl(a2, a3, off);
+  b.w3 = fsl(a3, 0u, off);
+  b.pos = 0;
+  b.len = len;
+  b.avail = 128 - (int)off;
+  b.src = p + 4;
+  if (len < 128) {
+    b.w0 &= top_mask(len);
+    b.w1 &= top_mask(len - 32);
+    b.w2 &= top_mask(len - 64);
+    b.w3 &= top_mask(len - 96);
+  }
+}
+
+WHFF_HD bool fits_no_refill(uint64_t bit, int len) { return (int)(bit & 31) + len <= 128; }
+
+// Window from one aligned 16-byte segment (FixedRate(8)).
+WHFF_HD void win_128(BitWin& b, uint32_t x, uint32_t y, uint32_t z, uint32_t w, int len) {
+  b.w0 = bswap32(x);
+  b.w1 = bswap32(y);
+  b.w2 = bswap32(z);
+  b.w3 = bswap32(w);
+  b.pos = 0;
+  b.len = len;
+  b.avail = 128;
+  b.src = nullptr;
+  if (len < 128) {
+    b.w0 &= top_mask(len);
+    b.w1 &= top_mask(len - 32);
+    b.w2 &= top_mask(len - 64);
+    b.w3 &= top_mask(len - 96);
+  }
+}
 
 template <bool REFILL>
-WHFF_HD void advance(BitWindow& b, uint32_t k) {  // k <= 32
-  b.off += k;
-  if (b.off >= 32) {
-    b.off -= 32;
-    b.w0 = b.w1;
-    b.w1 = b.w2;
-    b.w2 = b.w3;
-    if (REFILL) {
-      b.w3 = bswap32(ldg(b.src));
+WHFF_HD void adv(BitWin& b, uint32_t k) {  // k in [0, 32]
+  b.w0 = fsl(b.w0, b.w1, k);
+  b.w1 = fsl(b.w1, b.w2, k);
+  b.w2 = fsl(b.w2, b.w3, k);
+  b.w3 = fsl(b.w3, 0u, k);
+  b.pos += (int)k;
+  if (REFILL) {
+    b.avail -= (int)k;
+    if (b.avail < 96) {  // append the next word at register bit `avail`
+      const int q = b.pos + b.avail;           // its segment position
+      uint32_t wd = bswap32(ldg(b.src));
       b.src++;
-    } else {
-      b.w3 = 0;
+      wd &= top_mask(b.len - q);
+      const uint32_t sh = (uint32_t)(b.avail - 64);  // 0..31
+      b.w2 |= sh ? (wd >> sh) : wd;
+      b.w3 = fsl(wd, 0u, 32u - sh);
+      b.avail += 32;
     }
   }
 }
@@ -209,104 +268,11 @@ struct Decoded {
   int consumed;     // bits read (K:407)
 };
 
-struct ParseState {
-  uint32_t C[14];   // rank-space chunks: C[k] top lane = plane 26-2k, low lane = plane 25-2k
-  uint32_t sig;     // LSB orientation: bit c = coefficient c significant
-  uint32_t negm;
-  uint32_t nmask;   // ~(0xFFFFFFFF >> n): the top n bits
-  int n;
-  int pos;
-  bool done;
-};
-
 // insert a zero at rank r into both lanes of x (rank r at lane bit 15-r)
 WHFF_HD uint32_t insert_zero2(uint32_t x, uint32_t H) {
   uint32_t y = x & ~H;
   return x - y + (y >> 1);
 }
-
-template <int P, bool REFILL>
-WHFF_HD void plane_step(ParseState& st, BitWindow& bw, int len, int planes_limit) {
-  constexpr int K = (26 - P) >> 1;
-  constexpr bool TOP = ((26 - P) & 1) == 0;
-  if (st.done) return;
-  if (st.pos >= len || (26 - P) >= planes_limit) {  // K:323-325
-    st.done = true;
-    return;
-  }
-  const int n = st.n;
-  const uint32_t x = peek32(bw);
-  const int avail = len - st.pos;
-  if (avail < n) {  // refinement pass hits the limit (K:328-329)
-    uint32_t ch = x & ~(0xFFFFFFFFu >> avail);
-    if (TOP) st.C[K] = ch; else st.C[K] |= ch >> 16;
-    st.pos = len;
-    st.done = true;
-    return;
-  }
-  {
-    uint32_t ch = x & st.nmask;   // refinement chunk (K:326-332)
-    if (TOP) st.C[K] = ch; else st.C[K] |= ch >> 16;
-  }
-  if (n >= 16) {
-    advance<REFILL>(bw, (uint32_t)n);
-    st.pos += n;
-    return;
-  }
-  advance<REFILL>(bw, (uint32_t)n);
-  st.pos += n;
-  // significance pass (K:333-367)
-  uint32_t rem = ~st.sig & 0xFFFFu;
-  int krem = 16 - n;
-  while (krem > 0) {
-    if (st.pos >= len) { st.done = true; return; }
-    const uint32_t f = peek32(bw);
-    advance<REFILL>(bw, 1);
-    st.pos += 1;
-    if ((f >> 31) == 0) break;                     // group flag 0: plane ends
-    const uint32_t y = f << 1;
-    const int z = (int)clz32(y);                   // zero run before the hit
-    if (z >= krem) {                               // no hit in the remainder
-      if (len - st.pos < krem) { st.pos = len; st.done = true; return; }
-      advance<REFILL>(bw, (uint32_t)krem);
-      st.pos += krem;
-      break;
-    }
-    if (len - st.pos < z + 1) { st.pos = len; st.done = true; return; }
-    advance<REFILL>(bw, (uint32_t)(z + 1));
-    st.pos += z + 1;
-    if (st.pos >= len) { st.done = true; return; }  // sign unavailable (K:353-354)
-    const uint32_t s = (y << (z + 1)) >> 31;
-    advance<REFILL>(bw, 1);
-    st.pos += 1;
-    for (int i = 0; i < z; ++i) rem &= rem - 1;    // skip z insignificant
-    const uint32_t h = rem & (0u - rem);           // the hit
-    rem ^= h;                                      // drop the prefix (K:360-363)
-    krem -= z + 1;
-    const uint32_t r = popc32(st.sig & (h - 1));   // its rank
-    const uint32_t Ht = (0xFFFF0000u << (16 - r)) & 0xFFFF0000u;  // top r bits of a lane
-    const uint32_t H = Ht | (Ht >> 16);
-#pragma unroll
-    for (int k = 0; k <= K; ++k) st.C[k] = insert_zero2(st.C[k], H);
-    st.C[K] |= TOP ? (0x80000000u >> r) : (0x8000u >> r);  // significance bit p
-    st.sig |= h;
-    if (s) st.negm |= h;
-    st.n += 1;
-    st.nmask = ~(0xFFFFFFFFu >> st.n);
-  }
-}
-
-template <int P, bool REFILL>
-struct PlaneLoop {
-  WHFF_HD static void run(ParseState& st, BitWindow& bw, int len, int pl) {
-    plane_step<P, REFILL>(st, bw, len, pl);
-    PlaneLoop<P - 1, REFILL>::run(st, bw, len, pl);
-  }
-};
-template <bool REFILL>
-struct PlaneLoop<-1, REFILL> {
-  WHFF_HD static void run(ParseState&, BitWindow&, int, int) {}
-};
 
 // 16 plane words (two 16-bit lanes, see below) -> 16 magnitudes.
 // In: X[k] = W_k | W_{k+16} << 16 where W_p bit j = coefficient 15-j of plane p.
@@ -327,79 +293,159 @@ WHFF_HD void transpose16x32(uint32_t X[16]) {
 #undef WHFF_TSTAGE
 }
 
-// Parse one block segment of `len` bits.  n_planes is fixed at 27 (K:323).
+// Parse one block segment (the window's len bits); n_planes is 27 (K:323).
+//
+// The plane loop is a real loop (small code: the unrolled form overflowed the
+// instruction cache).  Refinement chunks are kept in rank space, two planes
+// per word: `cur` holds the pair being built, finished pairs go to the
+// per-thread array `pairs` (local memory, one store per two planes).  A hit
+// whose rank r is below the current count (an out-of-order significance)
+// inserts a zero at rank r into every stored pair and into `cur`; in-order
+// hits (r == n) need no insertion.  `lanes_mask` is the set of lanes calling
+// (for the warp-uniform early exit).
 template <bool HAS_RAW, bool REFILL>
-WHFF_HD void decode_block(BitWindow& bw, int len, int planes_limit, Decoded& d) {
+WHFF_HD void decode_block(BitWin& bw, int planes_limit, Decoded& d, unsigned lanes_mask) {
+  const int len = bw.len;
   d.negm = 0;
   d.emax = 0;
   d.raw = 0;
 #pragma unroll
   for (int c = 0; c < 16; ++c) d.mag[c] = 0;
+  bool header_done = true;
   if (len < 9) {                       // K:297-301: header truncated
     d.consumed = len < 0 ? 0 : len;
-    return;
+    header_done = false;
   }
-  const uint32_t hdr = peek32(bw);
-  const uint32_t code = hdr >> 23;
-  advance<REFILL>(bw, 9);
+  const uint32_t hdr = bw.w0;
+  const uint32_t code = header_done ? hdr >> 23 : 0u;
   d.emax = code;
-  int pos = 9;
-  if (HAS_RAW) {
-    if (len < 10) { d.consumed = 9; return; }
-    const uint32_t rf = (hdr >> 22) & 1u;
-    advance<REFILL>(bw, 1);
-    pos = 10;
-    if (rf) {                          // K:308-318 raw escape
-      d.raw = 1;
-      int nw = (len - 10) >> 5;
-      if (nw > 16) nw = 16;
+  if (HAS_RAW && header_done) {
+    if (len < 10) {
+      d.consumed = 9;
+      header_done = false;
+    } else {
+      adv<REFILL>(bw, 10);
+      if ((hdr >> 22) & 1u) {          // K:308-318 raw escape
+        d.raw = 1;
+        int nw = (len - 10) >> 5;
+        if (nw > 16) nw = 16;
 #pragma unroll
-      for (int c = 0; c < 16; ++c) {
-        if (c < nw) {
-          d.mag[c] = peek32(bw);
-          advance<REFILL>(bw, 32);
+        for (int c = 0; c < 16; ++c) {
+          if (c < nw) {
+            d.mag[c] = bw.w0;
+            adv<REFILL>(bw, 32);
+          }
         }
+        d.consumed = (len - 10 >= 512) ? 522 : len;
+        header_done = false;
       }
-      d.consumed = (len - 10 >= 512) ? 522 : len;
-      return;
+    }
+  } else if (header_done) {
+    adv<REFILL>(bw, 9);
+  }
+  if (header_done && code == 0) {
+    d.consumed = bw.pos;
+    header_done = false;
+  }
+  // lanes without a plane section still walk the (warp-uniform) loop with a
+  // zero window so the early-exit vote stays convergent
+  if (!header_done) {
+    bw.w0 = bw.w1 = bw.w2 = bw.w3 = 0u;
+    bw.len = 0;
+  }
+
+  uint32_t pairs[14];
+  uint32_t cur = 0;
+  uint32_t sig = 0, negm = 0;
+  uint32_t nmask = 0, flagbit = 0x80000000u, kq = 1;
+  int n = 0;
+  int nstored = 0;
+  bool killed = false;
+  const int pl = planes_limit < kNPlanes ? planes_limit : kNPlanes;
+  for (int t = 0; t < pl; ++t) {       // plane P = 26 - t (K:323)
+    const bool top = (t & 1) == 0;
+    const uint32_t x = bw.w0;
+    const uint32_t ch = x & nmask;     // refinement chunk (K:326-332)
+    cur = top ? ch : byte_perm(cur, ch, 0x3276);
+    if (x & flagbit) {                 // significance pass (K:333-367)
+      adv<REFILL>(bw, (uint32_t)(n + 1));
+      uint32_t rem = ~sig & 0xFFFFu;
+      int krem = 16 - n;
+      while (true) {
+        const uint32_t y = bw.w0;
+        const int z = (int)clz32(y);   // insignificant run before the hit
+        if (z >= krem) {               // no hit among the remainder
+          adv<REFILL>(bw, (uint32_t)krem);
+          break;
+        }
+        if (bw.pos + z + 1 >= bw.len) {  // sign unavailable: ignore, block ends
+          killed = true;
+          bw.w0 = bw.w1 = bw.w2 = bw.w3 = 0u;
+          bw.len = 0;
+          break;
+        }
+        const uint32_t sgn = (y << (z + 1)) >> 31;
+        if (z > 0) rem &= rem - 1;
+        if (z > 1) rem &= rem - 1;
+        for (int i = 2; i < z; ++i) rem &= rem - 1;  // skip z insignificant
+        const uint32_t h = rem & (0u - rem);          // the hit
+        rem ^= h;                                     // drop the prefix (K:360-363)
+        krem -= z + 1;
+        const uint32_t r = popc32(sig & (h - 1));    // its rank
+        if ((int)r < n) {                             // out of order: shift ranks >= r
+          const uint32_t Ht = (0xFFFF0000u << (16 - r)) & 0xFFFF0000u;
+          const uint32_t H = Ht | (Ht >> 16);
+          cur = insert_zero2(cur, H);
+          for (int j = 0; j < nstored; ++j) pairs[j] = insert_zero2(pairs[j], H);
+        }
+        cur |= top ? (0x80000000u >> r) : (0x8000u >> r);   // significance bit p
+        sig |= h;
+        if (sgn) negm |= h;
+        n += 1;
+        if (krem == 0) {               // remainder empty: no further flag
+          adv<REFILL>(bw, (uint32_t)(z + 2));
+          break;
+        }
+        const uint32_t f = (y << (z + 2)) >> 31;     // next group flag
+        adv<REFILL>(bw, (uint32_t)(z + 3));
+        if (!f) break;
+      }
+      nmask = top_mask(n);
+      flagbit = n < 16 ? (0x80000000u >> n) : 0u;
+      kq = (uint32_t)(n + (n < 16));
+    } else {
+      adv<REFILL>(bw, kq);             // quiet plane: chunk + flag 0
+    }
+    if (!top || t == pl - 1) pairs[nstored++] = cur;
+    if (__all_sync(lanes_mask, bw.pos >= bw.len)) {   // every lane past its data
+      if (top && t != pl - 1) pairs[nstored++] = cur;
+      break;
     }
   }
-  if (code == 0) { d.consumed = pos; return; }
-
-  ParseState st;
-#pragma unroll
-  for (int k = 0; k < 14; ++k) st.C[k] = 0;
-  st.sig = 0;
-  st.negm = 0;
-  st.nmask = 0;
-  st.n = 0;
-  st.pos = pos;
-  st.done = false;
-  PlaneLoop<26, REFILL>::run(st, bw, len, planes_limit);
-  d.consumed = st.pos;
-  d.negm = st.negm;
-  if (st.sig == 0) return;
+  if (!header_done) return;
+  d.consumed = killed ? len : (bw.pos < len ? bw.pos : len);
+  d.negm = negm;
+  if (sig == 0) return;
 
   // ranks -> coefficient indices (MSB orientation: bit 31-c = coefficient c)
-  const ExpandMasks e = expand_setup(brev32(st.sig));
+  const ExpandMasks e = expand_setup(brev32(sig));
+  uint32_t C[14];
 #pragma unroll
-  for (int k = 0; k < 14; ++k) st.C[k] = expand2(st.C[k], e);
-  // assemble X[k] = plane k (low half) | plane k+16 (high half); a lane value
-  // with bit (15-c) = coefficient c is the transpose's column order.
-  // plane p lives in C[(26-p)>>1], top lane iff (26-p) even.
+  for (int k = 0; k < 14; ++k) C[k] = k < nstored ? expand2(pairs[k], e) : 0u;
+  // X[k] = plane k (low half) | plane k+16 (high half); plane p lives in
+  // C[(26-p)>>1], top lane iff (26-p) even; lane bit (15-c) = coefficient c.
   uint32_t X[16];
 #pragma unroll
   for (int k = 0; k < 16; ++k) {
     const int pa = k, pb = k + 16;
     const int ka = (26 - pa) >> 1;
     const bool ta = ((26 - pa) & 1) == 0;
-    // low half <- lane of plane pa
-    uint32_t lo = ta ? (st.C[ka] >> 16) : (st.C[ka] & 0xFFFFu);
+    uint32_t lo = ta ? (C[ka] >> 16) : (C[ka] & 0xFFFFu);
     uint32_t hi = 0;
     if (pb <= 26) {
       const int kb = (26 - pb) >> 1;
       const bool tb = ((26 - pb) & 1) == 0;
-      hi = tb ? (st.C[kb] & 0xFFFF0000u) : (st.C[kb] << 16);
+      hi = tb ? (C[kb] & 0xFFFF0000u) : (C[kb] << 16);
     }
     X[k] = lo | hi;
   }

@@ -121,7 +121,9 @@ struct WordSink {
   uint64_t pos;      // absolute bit position of the next bit
   uint32_t acc;      // big-endian accumulator for word (pos >> 5)
   int n;
+  int limit;         // bits past the budget are dropped (K:266-270)
   WHFF_HD void put(uint32_t bit) {
+    if (n >= limit) return;
     acc |= (bit & 1u) << (31 - (uint32_t)(pos & 31));
     ++pos;
     ++n;

@@ -57,6 +57,8 @@ def hostcheck():
     L.hc_decompress.argtypes = [p, u64, p, p, i64, i64, ci, ci, p]
     L.hc_compress.argtypes = [p, i64, i64, ci, ctypes.c_double, p, p]
     L.hc_compress.restype = i64
+    L.hc_encode_blocks.argtypes = [p] * 6 + [i64, ci, ci, p, p]
+    L.hc_encode_blocks.restype = i64
     return L
 
 

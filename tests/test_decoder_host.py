@@ -135,3 +135,29 @@ def test_lift_range_fits_int32():
     bound = peak[0] * (2 ** 27 - 1) + 64      # + generous floor-rounding slack
     assert peak[0] == 15.0
     assert bound < 2 ** 31 - 1
+
+
+def test_device_encode_blocks_matches_oracle(hostcheck, orc):
+    """K:228-283 from coefficient arrays, including raw blocks truncated to a
+    fixed-rate budget (K:266-270)."""
+    rng = np.random.default_rng(1234)
+    for t in range(200):
+        nb = int(rng.integers(1, 50))
+        hr = bool(rng.integers(0, 2))
+        budget = int(rng.choice([0, 16 * int(rng.integers(1, 33))]))
+        mag = (rng.integers(0, 2 ** 27, (nb, 16)) >> rng.integers(0, 27, (nb, 16))).astype(np.uint32)
+        neg = rng.integers(0, 2, (nb, 16)).astype(np.uint8)
+        emax = rng.integers(0, 300, nb).astype(np.uint16)
+        emax[rng.random(nb) < .2] = 0
+        planes = rng.integers(0, 28, nb).astype(np.uint8)
+        raw = (rng.random(nb) < .2).astype(np.uint8)
+        rw = rng.integers(0, 2 ** 32, (nb, 16), dtype=np.uint64).astype(np.uint32)
+        want = orc.encode_blocks(mag, neg, emax, planes, raw, rw, 27, budget, hr)
+        offs = np.zeros(nb, np.uint64)
+        args = [P(mag), P(neg), P(emax), P(planes), P(raw), P(rw), nb, budget, int(hr), P(offs)]
+        tot = hostcheck.hc_encode_blocks(*args, None)
+        w = np.zeros(tot // 32 + 8, np.uint32)
+        hostcheck.hc_encode_blocks(*args, P(w))
+        assert tot == want[2]
+        assert np.array_equal(offs, want[1])
+        assert np.array_equal(w.view(np.uint8)[:(tot + 7) // 8], want[0])

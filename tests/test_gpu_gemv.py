@@ -1,0 +1,80 @@
+"""Dense GEMV policies on the GPU vs the reference (goldens, bit-exact for
+sequential and fixed-tree; blocked within the reference's own bound)."""
+
+import numpy as np
+import pytest
+
+pytestmark = pytest.mark.gpu
+
+SHAPES = (("sequential", 2), ("fixed-tree", 2), ("fixed-tree", 4), ("fixed-tree", 16))
+
+
+def test_gemv_bit_exact_vs_reference_goldens(golden):
+    from paper_1902_08018_b200.mpgemv import GemvRequest, gemv
+    g = golden("gemv_cases")
+    for i in range(int(g["n"][0])):
+        k = f"g{i:02d}"
+        m, v = g[k + "_m"], g[k + "_v"]
+        for pol in ("mixed", "single", "double"):
+            for shape, fo in SHAPES:
+                got = gemv(GemvRequest(m, v, pol, shape, fo))
+                assert got.dtype == np.float32
+                assert np.array_equal(got.view(np.uint32), g[f"{k}_{pol}_{shape}_{fo}"].view(np.uint32)), \
+                    (k, pol, shape, fo)
+
+
+def test_gemv_oracle_matches_reference(golden):
+    from paper_1902_08018_b200.mpgemv import gemv_oracle
+    g = golden("gemv_cases")
+    for i in range(int(g["n"][0])):
+        k = f"g{i:02d}"
+        assert np.array_equal(gemv_oracle(g[k + "_m"], g[k + "_v"]), g[k + "_oracle"])
+
+
+def test_blocked_within_reference_bound(rng):
+    """tests/test_mpgemv.py:116-130 bound for the B200 blocked order."""
+    from paper_1902_08018_b200.mpgemv import GemvRequest, gemv, gemv_oracle
+    for dims in ((1, 1), (7, 130), (64, 1031), (378, 16384), (3, 262147)):
+        m = rng.standard_normal(dims).astype(np.float32)
+        v = rng.standard_normal(dims[1]).astype(np.float32)
+        ref = gemv_oracle(m, v)
+        scale = np.abs(m).astype(np.float64) @ np.abs(v).astype(np.float64)
+        bound = (dims[1] + 1) * np.finfo(np.float32).eps * np.maximum(scale, np.abs(ref))
+        for pol in ("mixed", "single", "double"):
+            got = gemv(GemvRequest(m, v, pol, "blocked"))
+            assert (np.abs(got.astype(np.float64) - ref) <= bound + 1e-300).all(), (dims, pol)
+
+
+def test_mixed_beats_single_on_wide_rows(rng):
+    from paper_1902_08018_b200.mpgemv import GemvRequest, gemv, gemv_oracle, relative_error
+    m = rng.standard_normal((32, 8192)).astype(np.float32)
+    v = rng.standard_normal(8192).astype(np.float32)
+    ref = gemv_oracle(m, v)
+    em = relative_error(gemv(GemvRequest(m, v, "mixed", "sequential")), ref)
+    es = relative_error(gemv(GemvRequest(m, v, "single", "sequential")), ref)
+    assert np.median(em) < np.median(es)
+
+
+def test_gemv_input_validation(rng):
+    from paper_1902_08018_b200.errors import DimensionError, NonFiniteError, WhffError
+    from paper_1902_08018_b200.mpgemv import GemvRequest, gemv
+    m = rng.standard_normal((2, 3)).astype(np.float32)
+    with pytest.raises(DimensionError):
+        gemv(GemvRequest(m, np.zeros(4, np.float32)))
+    bad = m.copy()
+    bad[1, 2] = np.inf
+    with pytest.raises(NonFiniteError) as exc:
+        gemv(GemvRequest(bad, np.zeros(3, np.float32)))
+    assert exc.value.name == "matrix" and exc.value.index == 5
+    with pytest.raises(WhffError):
+        GemvRequest(m, m[0], "half")
+    with pytest.raises(WhffError):
+        GemvRequest(m, m[0], "mixed", "fixed-tree", fanout=3)
+
+
+def test_plugin_gemv_kernel_matches_compiled_reference(golden):
+    from paper_1902_08018_b200 import backend
+    g = golden("gemv_cases")
+    k = "g02"
+    got = backend.gemv_kernel(g[k + "_m"], g[k + "_v"], "mixed", "fixed-tree", 16)
+    assert np.array_equal(got, g[f"{k}_mixed_fixed-tree_16"])

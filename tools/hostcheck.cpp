@@ -18,13 +18,18 @@ void hc_decode_blocks(const uint32_t* words, uint64_t payload_bits,
     if (limit > payload_bits) limit = payload_bits;
     int64_t len64 = (int64_t)limit - (int64_t)start;
     int len = len64 > 65535 ? 65535 : (int)len64;
-    whff::BitWindow bw;
-    whff::window_at(bw, words, start);
+    whff::BitWin bw;
+    whff::win_at(bw, words, start, len);
     whff::Decoded d;
-    if (has_raw)
-      whff::decode_block<true, true>(bw, len, planes_limit, d);
-    else
-      whff::decode_block<false, true>(bw, len, planes_limit, d);
+    // the kernels' dispatch: no refill when the segment fits the register
+    const bool fits = whff::fits_no_refill(start, len);
+    if (has_raw) {
+      if (!fits) whff::decode_block<true, true>(bw, planes_limit, d, 1u);
+      else whff::decode_block<true, false>(bw, planes_limit, d, 1u);
+    } else {
+      if (!fits) whff::decode_block<false, true>(bw, planes_limit, d, 1u);
+      else whff::decode_block<false, false>(bw, planes_limit, d, 1u);
+    }
     emax[b] = (uint16_t)d.emax;
     raw[b] = (uint8_t)d.raw;
     consumed[b] = (uint64_t)d.consumed;
@@ -53,13 +58,13 @@ void hc_decompress(const uint32_t* words, uint64_t payload_bits,
     if (limit > payload_bits) limit = payload_bits;
     int64_t len64 = (int64_t)limit - (int64_t)start;
     int len = len64 > 65535 ? 65535 : (int)len64;
-    whff::BitWindow bw;
-    whff::window_at(bw, words, start);
+    whff::BitWin bw;
+    whff::win_at(bw, words, start, len);
     whff::Decoded d;
-    if (has_raw)
-      whff::decode_block<true, true>(bw, len, planes_limit, d);
+    if (has_raw)   // always the refill path here
+      whff::decode_block<true, true>(bw, planes_limit, d, 1u);
     else
-      whff::decode_block<false, true>(bw, len, planes_limit, d);
+      whff::decode_block<false, true>(bw, planes_limit, d, 1u);
     float blk[16];
     whff::reconstruct_words(d, blk);
     int64_t r0 = (b / bc) * 4, c0 = (b % bc) * 4;
@@ -88,7 +93,7 @@ int64_t hc_compress(const float* a, int64_t rows, int64_t cols, int mode, double
     offsets[b] = total;
     int n;
     if (words) {
-      whff::WordSink ws{words, total, 0u, 0};
+      whff::WordSink ws{words, total, 0u, 0, budget ? budget : 0x7FFFFFFF};
       n = whff::encode_one(pl.mag, pl.negm, pl.code, pl.planes, pl.raw, pl.raw_words,
                            budget, has_raw, ws);
       ws.finish();
@@ -96,6 +101,37 @@ int64_t hc_compress(const float* a, int64_t rows, int64_t cols, int mode, double
       whff::CountSink cs;
       n = whff::encode_one(pl.mag, pl.negm, pl.code, pl.planes, pl.raw, pl.raw_words,
                            budget, has_raw, cs);
+    }
+    if (budget) n = budget;
+    total += (uint64_t)n;
+  }
+  return (int64_t)total;
+}
+}
+
+extern "C" {
+// K:228-283 encode_blocks from arrays with the device encoder logic.
+int64_t hc_encode_blocks(const uint32_t* mag, const uint8_t* neg, const uint16_t* emax,
+                         const uint8_t* planes, const uint8_t* raw_mask, const uint32_t* raw_words,
+                         int64_t nb, int budget, int has_raw, uint64_t* offsets, uint32_t* words) {
+  uint64_t total = 0;
+  for (int64_t b = 0; b < nb; ++b) {
+    uint32_t m[16], rw[16], negm = 0;
+    for (int c = 0; c < 16; ++c) {
+      m[c] = mag[16 * b + c];
+      rw[c] = raw_words[16 * b + c];
+      if (neg[16 * b + c]) negm |= 1u << c;
+    }
+    bool raw = has_raw && raw_mask[b];
+    offsets[b] = total;
+    int n;
+    if (words) {
+      whff::WordSink ws{words, total, 0u, 0, budget ? budget : 0x7FFFFFFF};
+      n = whff::encode_one(m, negm, emax[b], planes[b], raw, rw, budget, has_raw != 0, ws);
+      ws.finish();
+    } else {
+      whff::CountSink cs;
+      n = whff::encode_one(m, negm, emax[b], planes[b], raw, rw, budget, has_raw != 0, cs);
     }
     if (budget) n = budget;
     total += (uint64_t)n;
