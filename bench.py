@@ -287,8 +287,8 @@ def reference_main(args, world, rank):
     paths = make_cpu_samples(args, tmp)
     # each step = one pass over the 3-axis sample on all cores
     cores = len(os.sched_getaffinity(0)) if hasattr(os, "sched_getaffinity") else os.cpu_count()
-    reps = max(1, cores // 3)
-    for _ in range(args.warmup):
+    reps = max(1, (5 * cores) // 6)
+    for _ in range(min(args.warmup, 1)):
         run_cpu_leg(paths, 1)
     times, gbs = [], []
     total_bytes = 0
@@ -442,9 +442,10 @@ def b200_main(args, world, rank, local):
         tmp = tempfile.mkdtemp()
         paths = make_cpu_samples(args, tmp)
         cores = len(os.sched_getaffinity(0)) if hasattr(os, "sched_getaffinity") else os.cpu_count()
-        v, wall, cores, kind, per, _ = run_cpu_leg(paths, max(1, cores // 3))
+        reps = max(1, (5 * cores) // 6)          # ~2.5 chunks per core: 10-30 core-seconds
+        v, wall, cores, kind, per, _ = run_cpu_leg(paths, reps)
         cpu = {"value": round(v, 6), "unit": "GB/s", "cores": cores, "kind": kind,
-               "sample": f"{3 * max(1, cores // 3)} chunks of {args.rows}x{args.cpu_sample_cols} "
+               "sample": f"{3 * reps} chunks of {args.rows}x{args.cpu_sample_cols} "
                          f"({args.mode}), reference codec.decompress + mpgemv.gemv(mixed, sequential); "
                          f"{wall:.1f}s wall"}
 

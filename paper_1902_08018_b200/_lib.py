@@ -14,7 +14,7 @@ import threading
 from .errors import CorruptStreamError, DimensionError, NonFiniteError, WhffError
 
 HERE = os.path.dirname(os.path.abspath(__file__))
-LIB_PATH = os.path.join(HERE, "libwhff_b200.so")
+LIB_PATH = os.environ.get("WHFF_LIB", os.path.join(HERE, "libwhff_b200.so"))
 
 OK, E_DIM, E_NONFINITE, E_CORRUPT, E_ARG, E_OVERFLOW, E_NOMEM, E_CUDA = range(8)
 MODE_RATE, MODE_PRECISION, MODE_ACCURACY = 0, 1, 2

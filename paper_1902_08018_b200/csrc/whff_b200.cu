@@ -267,14 +267,21 @@ struct Acc {
   float probe;   // single policy: NaN iff a decoded value was non-finite
 };
 
-__device__ __forceinline__ void acc_exact(Acc& A, int policy, const float x[16], float4 v4,
+__device__ __forceinline__ void acc_exact(Acc& A, int policy, const float x_in[16], float4 v4,
                                           uint32_t colmask) {
   const float vv[4] = {v4.x, v4.y, v4.z, v4.w};
+  float x[16];
+#pragma unroll
+  for (int k = 0; k < 16; ++k) x[k] = x_in[k];
+  if (colmask != 0xFu) {          // last block-column: padded columns contribute nothing
+#pragma unroll
+    for (int k = 0; k < 16; ++k)
+      if (!((colmask >> (k & 3)) & 1u)) x[k] = 0.0f;
+  }
 #pragma unroll
   for (int i = 0; i < 4; ++i) {
 #pragma unroll
     for (int j = 0; j < 4; ++j) {
-      if (!((colmask >> j) & 1u)) continue;
       const float xv = x[4 * i + j];
       if (policy == WHFF_POLICY_MIXED) {
         A.d[i] = __dadd_rn(A.d[i], (double)__fmul_rn(xv, vv[j]));
@@ -320,9 +327,16 @@ template <> struct VarTraits<2> { static constexpr bool kRefill = true, kRaw = f
 template <> struct VarTraits<3> { static constexpr bool kRefill = true, kRaw = true, kIndexed = true; };
 
 constexpr int kGemvWarps = 8;
+// launch bounds: plain 256 lets ptxas settle at 64 registers (4 CTAs/SM),
+// measured best for the fused kernel; -DWHFF_GEMV_MINB=n overrides for sweeps
+#ifdef WHFF_GEMV_MINB
+#define WHFF_GEMV_LB __launch_bounds__(256, WHFF_GEMV_MINB)
+#else
+#define WHFF_GEMV_LB __launch_bounds__(256)
+#endif
 
 template <int VAR, int EVAL>
-__global__ void __launch_bounds__(256) k_decode_gemv(JobTable T, int policy,
+__global__ void WHFF_GEMV_LB k_decode_gemv(JobTable T, int policy,
                                                      unsigned long long* status) {
   using TR = VarTraits<VAR>;
   // one CTA per (job, block-row); its 8 warps split the row's 32-block groups
@@ -380,7 +394,7 @@ __global__ void __launch_bounds__(256) k_decode_gemv(JobTable T, int policy,
       const uint64_t bn = bcol + 32 * kGemvWarps;
       if (bn < bc) nxt = ldg(seg128 + row_block0 + bn);   // prefetch this warp's next group
       win_128(bw, q.x, q.y, q.z, q.w, active ? clamp_len(b * 128ull, 128ull, s.payload_bits) : 0);
-      decode_block<false, false>(bw, pl, d, 0xFFFFFFFFu);
+      decode_block<false, false, false>(bw, pl, d, 0xFFFFFFFFu);
     } else {
       uint64_t start = 0;
       int len = 0;

@@ -293,6 +293,79 @@ WHFF_HD void transpose16x32(uint32_t X[16]) {
 #undef WHFF_TSTAGE
 }
 
+// One plane of the parse (K:323-367); TOP = the plane is the high lane of its
+// pair word.  Refinement chunks stay in rank space (bit 31-r / 15-r = rank r).
+template <bool REFILL>
+struct PlaneParser {
+  BitWin& bw;
+  uint32_t* pairs;
+  uint32_t cur = 0, sig = 0, negm = 0;
+  uint32_t nmask = 0, flagbit = 0x80000000u, kq = 1;
+  int n = 0;
+  bool killed = false;
+  WHFF_HD PlaneParser(BitWin& b, uint32_t* p) : bw(b), pairs(p) {}
+
+  template <bool TOP>
+  WHFF_HD void plane(int t) {
+    const uint32_t x = bw.w0;
+    const uint32_t ch = x & nmask;     // refinement chunk (K:326-332)
+    cur = TOP ? ch : byte_perm(cur, ch, 0x3276);
+    if (!(x & flagbit)) {              // quiet plane: chunk + group flag 0
+      adv<REFILL>(bw, kq);
+      return;
+    }
+    adv<REFILL>(bw, (uint32_t)(n + 1));   // significance pass (K:333-367)
+    uint32_t rem = ~sig & 0xFFFFu;
+    int krem = 16 - n;
+    while (true) {
+      const uint32_t y = bw.w0;
+      const int z = (int)clz32(y);     // insignificant run before the hit
+      if (z >= krem) {                 // no hit among the remainder
+        adv<REFILL>(bw, (uint32_t)krem);
+        break;
+      }
+      if (bw.pos + z + 1 >= bw.len) {  // sign unavailable: ignore, block ends
+        killed = true;
+        bw.w0 = bw.w1 = bw.w2 = bw.w3 = 0u;
+        bw.len = 0;
+        break;
+      }
+      const uint32_t sgn = (y << (z + 1)) >> 31;
+      if (z > 0) rem &= rem - 1;       // skip z insignificant
+      if (z > 1) rem &= rem - 1;
+      if (z > 2) rem &= rem - 1;
+      if (z > 3) {
+        rem &= rem - 1;
+        for (int i = 4; i < z; ++i) rem &= rem - 1;
+      }
+      const uint32_t h = rem & (0u - rem);          // the hit
+      rem ^= h;                                     // drop the prefix (K:360-363)
+      krem -= z + 1;
+      const uint32_t r = popc32(sig & (h - 1));    // its rank
+      if ((int)r < n) {                             // out of order: shift ranks >= r
+        const uint32_t Ht = (0xFFFF0000u << (16 - r)) & 0xFFFF0000u;
+        const uint32_t H = Ht | (Ht >> 16);
+        cur = insert_zero2(cur, H);
+        for (int j = 0; j < (t >> 1); ++j) pairs[j] = insert_zero2(pairs[j], H);
+      }
+      cur |= (TOP ? 0x80000000u : 0x8000u) >> r;   // significance bit p
+      sig |= h;
+      if (sgn) negm |= h;
+      n += 1;
+      if (krem == 0) {                 // remainder empty: no further flag
+        adv<REFILL>(bw, (uint32_t)(z + 2));
+        break;
+      }
+      const uint32_t f = (y << (z + 2)) >> 31;     // next group flag
+      adv<REFILL>(bw, (uint32_t)(z + 3));
+      if (!f) break;
+    }
+    nmask = top_mask(n);
+    flagbit = n < 16 ? (0x80000000u >> n) : 0u;
+    kq = (uint32_t)(n + (n < 16));
+  }
+};
+
 // Parse one block segment (the window's len bits); n_planes is 27 (K:323).
 //
 // The plane loop is a real loop (small code: the unrolled form overflowed the
@@ -303,7 +376,7 @@ WHFF_HD void transpose16x32(uint32_t X[16]) {
 // inserts a zero at rank r into every stored pair and into `cur`; in-order
 // hits (r == n) need no insertion.  `lanes_mask` is the set of lanes calling
 // (for the warp-uniform early exit).
-template <bool HAS_RAW, bool REFILL>
+template <bool HAS_RAW, bool REFILL, bool EARLY_EXIT = true>
 WHFF_HD void decode_block(BitWin& bw, int planes_limit, Decoded& d, unsigned lanes_mask) {
   const int len = bw.len;
   d.negm = 0;
@@ -355,73 +428,25 @@ WHFF_HD void decode_block(BitWin& bw, int planes_limit, Decoded& d, unsigned lan
   }
 
   uint32_t pairs[14];
-  uint32_t cur = 0;
-  uint32_t sig = 0, negm = 0;
-  uint32_t nmask = 0, flagbit = 0x80000000u, kq = 1;
-  int n = 0;
-  int nstored = 0;
-  bool killed = false;
+  PlaneParser<REFILL> pp(bw, pairs);
   const int pl = planes_limit < kNPlanes ? planes_limit : kNPlanes;
-  for (int t = 0; t < pl; ++t) {       // plane P = 26 - t (K:323)
-    const bool top = (t & 1) == 0;
-    const uint32_t x = bw.w0;
-    const uint32_t ch = x & nmask;     // refinement chunk (K:326-332)
-    cur = top ? ch : byte_perm(cur, ch, 0x3276);
-    if (x & flagbit) {                 // significance pass (K:333-367)
-      adv<REFILL>(bw, (uint32_t)(n + 1));
-      uint32_t rem = ~sig & 0xFFFFu;
-      int krem = 16 - n;
-      while (true) {
-        const uint32_t y = bw.w0;
-        const int z = (int)clz32(y);   // insignificant run before the hit
-        if (z >= krem) {               // no hit among the remainder
-          adv<REFILL>(bw, (uint32_t)krem);
-          break;
-        }
-        if (bw.pos + z + 1 >= bw.len) {  // sign unavailable: ignore, block ends
-          killed = true;
-          bw.w0 = bw.w1 = bw.w2 = bw.w3 = 0u;
-          bw.len = 0;
-          break;
-        }
-        const uint32_t sgn = (y << (z + 1)) >> 31;
-        if (z > 0) rem &= rem - 1;
-        if (z > 1) rem &= rem - 1;
-        for (int i = 2; i < z; ++i) rem &= rem - 1;  // skip z insignificant
-        const uint32_t h = rem & (0u - rem);          // the hit
-        rem ^= h;                                     // drop the prefix (K:360-363)
-        krem -= z + 1;
-        const uint32_t r = popc32(sig & (h - 1));    // its rank
-        if ((int)r < n) {                             // out of order: shift ranks >= r
-          const uint32_t Ht = (0xFFFF0000u << (16 - r)) & 0xFFFF0000u;
-          const uint32_t H = Ht | (Ht >> 16);
-          cur = insert_zero2(cur, H);
-          for (int j = 0; j < nstored; ++j) pairs[j] = insert_zero2(pairs[j], H);
-        }
-        cur |= top ? (0x80000000u >> r) : (0x8000u >> r);   // significance bit p
-        sig |= h;
-        if (sgn) negm |= h;
-        n += 1;
-        if (krem == 0) {               // remainder empty: no further flag
-          adv<REFILL>(bw, (uint32_t)(z + 2));
-          break;
-        }
-        const uint32_t f = (y << (z + 2)) >> 31;     // next group flag
-        adv<REFILL>(bw, (uint32_t)(z + 3));
-        if (!f) break;
-      }
-      nmask = top_mask(n);
-      flagbit = n < 16 ? (0x80000000u >> n) : 0u;
-      kq = (uint32_t)(n + (n < 16));
-    } else {
-      adv<REFILL>(bw, kq);             // quiet plane: chunk + flag 0
-    }
-    if (!top || t == pl - 1) pairs[nstored++] = cur;
-    if (__all_sync(lanes_mask, bw.pos >= bw.len)) {   // every lane past its data
-      if (top && t != pl - 1) pairs[nstored++] = cur;
+  int t = 0;                           // planes processed (plane P = 26 - t, K:323)
+  for (int t2 = 0; t2 < 14; ++t2) {    // two planes per iteration: one word of pairs
+    if (t >= pl) break;
+    pp.template plane<true>(t);
+    if (t + 1 >= pl) {                 // odd plane count: lone top lane
+      pairs[t2] = pp.cur;
+      t += 1;
       break;
     }
+    pp.template plane<false>(t + 1);
+    pairs[t2] = pp.cur;
+    t += 2;
+    if (EARLY_EXIT && __all_sync(lanes_mask, bw.pos >= bw.len)) break;  // all lanes past their data
   }
+  const int nstored = (t + 1) >> 1;
+  const bool killed = pp.killed;
+  const uint32_t sig = pp.sig, negm = pp.negm;
   if (!header_done) return;
   d.consumed = killed ? len : (bw.pos < len ? bw.pos : len);
   d.negm = negm;

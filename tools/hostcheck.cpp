@@ -61,10 +61,10 @@ void hc_decompress(const uint32_t* words, uint64_t payload_bits,
     whff::BitWin bw;
     whff::win_at(bw, words, start, len);
     whff::Decoded d;
-    if (has_raw)   // always the refill path here
-      whff::decode_block<true, true>(bw, planes_limit, d, 1u);
+    if (has_raw)   // always the refill path here, without the early exit
+      whff::decode_block<true, true, false>(bw, planes_limit, d, 1u);
     else
-      whff::decode_block<false, true>(bw, planes_limit, d, 1u);
+      whff::decode_block<false, true, false>(bw, planes_limit, d, 1u);
     float blk[16];
     whff::reconstruct_words(d, blk);
     int64_t r0 = (b / bc) * 4, c0 = (b % bc) * 4;
