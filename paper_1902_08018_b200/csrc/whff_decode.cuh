@@ -191,12 +191,62 @@ WHFF_HD void win_128(BitWin& b, uint32_t x, uint32_t y, uint32_t z, uint32_t w, 
   }
 }
 
+// 128-bit left shift by k < 32 as a chain of 32x32->64 multiply-adds by 2^k:
+// (w_i * 2^k + hi(w_{i+1} * 2^k)) runs on the FMA pipe (IMAD.WIDE), leaving
+// the ALU pipe -- the decoder's bottleneck -- one shift instead of four.
+// x >> J (0 < J < 32, constant) as mul.hi(x, 2^(32-J)): IMAD.HI on the FMA pipe
+#ifndef WHFF_SHR_FMA
+#define WHFF_SHR_FMA 0
+#endif
+#ifndef WHFF_ADV_IMAD
+#define WHFF_ADV_IMAD 0
+#endif
+template <int J>
+WHFF_HD uint32_t shr_fma(uint32_t x) {
+#if defined(__CUDA_ARCH__) && WHFF_SHR_FMA
+  uint32_t d;
+  asm("mul.hi.u32 %0, %1, %2;" : "=r"(d) : "r"(x), "n"(1u << (32 - J)));
+  return d;
+#else
+  return x >> J;
+#endif
+}
+WHFF_HD uint64_t mad_wide(uint32_t a, uint32_t b, uint64_t c) {
+#if defined(__CUDA_ARCH__)
+  uint64_t d;
+  asm("mad.wide.u32 %0, %1, %2, %3;" : "=l"(d) : "r"(a), "r"(b), "l"(c));
+  return d;
+#else
+  return (uint64_t)a * b + c;
+#endif
+}
+WHFF_HD void shl128(BitWin& b, uint32_t k) {
+  const uint32_t p = 1u << k;
+  const uint64_t t3 = mad_wide(b.w3, p, 0ull);
+  const uint64_t t2 = mad_wide(b.w2, p, t3 >> 32);
+  const uint64_t t1 = mad_wide(b.w1, p, t2 >> 32);
+  const uint64_t t0 = mad_wide(b.w0, p, t1 >> 32);
+  b.w3 = (uint32_t)t3;
+  b.w2 = (uint32_t)t2;
+  b.w1 = (uint32_t)t1;
+  b.w0 = (uint32_t)t0;
+}
+
 template <bool REFILL>
 WHFF_HD void adv(BitWin& b, uint32_t k) {  // k in [0, 32]
-  b.w0 = fsl(b.w0, b.w1, k);
-  b.w1 = fsl(b.w1, b.w2, k);
-  b.w2 = fsl(b.w2, b.w3, k);
-  b.w3 = fsl(b.w3, 0u, k);
+  if (WHFF_ADV_IMAD && k < 32) {
+    shl128(b, k);
+  } else if (!WHFF_ADV_IMAD) {
+    b.w0 = fsl(b.w0, b.w1, k);
+    b.w1 = fsl(b.w1, b.w2, k);
+    b.w2 = fsl(b.w2, b.w3, k);
+    b.w3 = fsl(b.w3, 0u, k);
+  } else {
+    b.w0 = b.w1;
+    b.w1 = b.w2;
+    b.w2 = b.w3;
+    b.w3 = 0u;
+  }
   b.pos += (int)k;
   if (REFILL) {
     b.avail -= (int)k;
@@ -249,10 +299,10 @@ WHFF_HD ExpandMasks expand_setup(uint32_t m16_msb) {  // mask in bits 31..16
 
 WHFF_HD uint32_t expand2(uint32_t x, const ExpandMasks& e) {
   uint32_t t;
-  t = x >> 8; x = (x & ~e.v3) | (t & e.v3);
-  t = x >> 4; x = (x & ~e.v2) | (t & e.v2);
-  t = x >> 2; x = (x & ~e.v1) | (t & e.v1);
-  t = x >> 1; x = (x & ~e.v0) | (t & e.v0);
+  t = shr_fma<8>(x); x = (x & ~e.v3) | (t & e.v3);
+  t = shr_fma<4>(x); x = (x & ~e.v2) | (t & e.v2);
+  t = shr_fma<2>(x); x = (x & ~e.v1) | (t & e.v1);
+  t = shr_fma<1>(x); x = (x & ~e.v0) | (t & e.v0);
   return x & e.m;
 }
 
@@ -281,7 +331,7 @@ WHFF_HD void transpose16x32(uint32_t X[16]) {
 #define WHFF_TSTAGE(J, M)                                            \
   _Pragma("unroll") for (int k = 0; k < 16; ++k) {                   \
     if ((k & (J)) == 0) {                                            \
-      uint32_t t = ((X[k] >> (J)) ^ X[k + (J)]) & (M);               \
+      uint32_t t = (shr_fma<J>(X[k]) ^ X[k + (J)]) & (M);             \
       X[k] ^= t << (J);                                              \
       X[k + (J)] ^= t;                                               \
     }                                                                \
