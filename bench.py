@@ -41,6 +41,9 @@ def parse():
     ap.add_argument("--impl", default="b200", choices=["b200", "reference"])
     ap.add_argument("--mode", default="rate:8", help="rate:BPV | precision:P | accuracy:TOL")
     ap.add_argument("--evaluation", default="exact", choices=["exact", "coefficient"])
+    ap.add_argument("--layout", default="skeleton-first", choices=["reference", "skeleton-first"],
+                    help="device payload layout (whff_dstream_relayout): a per-block bit "
+                         "permutation of the WHFZ stream, same bytes, same decoded words")
     ap.add_argument("--policy", default="mixed", choices=["mixed", "single", "double"])
     ap.add_argument("--slits", type=int, default=52)
     ap.add_argument("--rows", type=int, default=378)
@@ -170,6 +173,8 @@ def build_field(args, world, rank):
             rows = synth.deformation_rows(spec, a, ops.phases[synth.AXES[a]], src * args.rows,
                                           (src + 1) * args.rows, device="cuda")
             made[(a, src)] = codec.compress_device(rows, mode)
+            if args.layout != "reference":
+                made[(a, src)].relayout(args.layout)
             del rows
             streams[a][src] = made[(a, src)]
         if streams[a][s] is None:
@@ -466,7 +471,8 @@ def b200_main(args, world, rank, local):
     try:
         with open(os.path.join(ROOT, "profiles", "ncu_traffic.json")) as fh:
             tj = json.load(fh)
-            if tj.get("mode") == args.mode and tj.get("evaluation") == args.evaluation:
+            if (tj.get("mode") == args.mode and tj.get("evaluation") == args.evaluation
+                    and tj.get("layout", "reference") == args.layout):
                 traffic = tj.get("dram_bytes_per_launch")
     except Exception:
         pass
@@ -484,6 +490,7 @@ def b200_main(args, world, rank, local):
         "config": {"workload": "paper-scale WHFF step (configs[2]): thermal T=608^2 nnz7 + "
                                f"3 axes x {args.slits} slits x {args.rows}x{args.S}",
                    "mode": args.mode, "evaluation": args.evaluation, "policy": args.policy,
+                   "layout": args.layout,
                    "parallelism": f"row-shard{world}" if world > 1 else "single",
                    "vector_mode": args.vector_mode if world > 1 else None,
                    "l2": "inputs (compressed field) far larger than L2; no flush needed",

@@ -73,6 +73,13 @@ typedef enum whff_eval {
   WHFF_EVAL_EXACT = 0, /* bit-exact decoded words x, binary32 products x*v    */
   WHFF_EVAL_COEFF = 1  /* coefficient domain: y = G * sum 2^(e-26) Q (G^T v)  */
 } whff_eval_t;
+/* device payload layout (whff_dstream_relayout) */
+typedef enum whff_layout {
+  WHFF_LAYOUT_REFERENCE = 0,      /* WHFZ bytes as produced by codec.compress        */
+  WHFF_LAYOUT_SKELETON_FIRST = 1  /* per-block bit permutation: header, significance
+                                     skeleton, then refinement bits per coefficient;
+                                     same bytes/index, decodes to identical words    */
+} whff_layout_t;
 /* device index layout chosen at stream creation */
 typedef enum whff_index_kind {
   WHFF_INDEX_IMPLICIT = 0, /* fixed rate, offsets b*16*bpv: no index bytes   */
@@ -91,6 +98,7 @@ typedef struct whff_dstream_info {
   uint64_t device_bytes;   /* all device memory owned by the stream           */
   int32_t planes_limit;
   int32_t has_raw_flag;
+  int32_t layout;          /* whff_layout_t */
 } whff_dstream_info_t;
 
 int whff_abi_version(void);
@@ -120,6 +128,10 @@ whff_status_t whff_dstream_create_segments(int device, const uint8_t* payload_ho
                                            int planes_limit, int has_raw_flag,
                                            whff_dstream_t* out);
 whff_status_t whff_dstream_destroy(whff_dstream_t s);
+/* Re-lay the device payload out in place (forward or inverse permutation of
+ * every block segment, computed by the reference parse on the device).
+ * Needs an implicit or compact index (disjoint segments).  Synchronous.    */
+whff_status_t whff_dstream_relayout(whff_dstream_t s, int layout, whff_stream_t stream);
 /* Physically distinct device copy of a stream (same device).  Synchronous. */
 whff_status_t whff_dstream_clone(whff_dstream_t s, whff_dstream_t* out);
 whff_status_t whff_dstream_get_info(whff_dstream_t s, whff_dstream_info_t* info);

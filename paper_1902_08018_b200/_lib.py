@@ -22,6 +22,8 @@ POLICY = {"mixed": 0, "single": 1, "double": 2}
 SHAPE = {"sequential": 0, "fixed-tree": 1, "blocked": 2}
 EVAL = {"exact": 0, "coefficient": 1}
 INDEX_KIND = {0: "implicit", 1: "compact", 2: "full"}
+LAYOUT = {"reference": 0, "skeleton-first": 1}
+LAYOUT_NAME = {v: k for k, v in LAYOUT.items()}
 STATUS_CLEAR = -1  # UINT64_MAX viewed as int64
 
 
@@ -32,7 +34,7 @@ class DStreamInfo(ctypes.Structure):
                 ("payload_bytes", ctypes.c_uint64), ("total_bits", ctypes.c_uint64),
                 ("index_bytes", ctypes.c_uint64),
                 ("device_bytes", ctypes.c_uint64), ("planes_limit", ctypes.c_int32),
-                ("has_raw_flag", ctypes.c_int32)]
+                ("has_raw_flag", ctypes.c_int32), ("layout", ctypes.c_int32)]
 
 
 _P = ctypes.c_void_p
@@ -46,6 +48,7 @@ _SIG = {
     "whff_dstream_create_segments": ([_I, _P, _U64, _P, _P, _U64, _I, _I, _P], _I),
     "whff_dstream_destroy": ([_P], _I),
     "whff_dstream_clone": ([_P, _P], _I),
+    "whff_dstream_relayout": ([_P, _I, _P], _I),
     "whff_dstream_get_info": ([_P, _P], _I),
     "whff_dstream_download": ([_P, _P, _P], _I),
     "whff_compress": ([_P, _U64, _U64, _U64, _I, ctypes.c_double, _P, _P], _I),

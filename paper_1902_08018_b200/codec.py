@@ -153,6 +153,7 @@ class DeviceStream:
         self.index_kind = _lib.INDEX_KIND[int(info.index_kind)]
         self.planes_limit = int(info.planes_limit)
         self.has_raw_flag = bool(info.has_raw_flag)
+        self.layout = _lib.LAYOUT_NAME[int(info.layout)]
         self.total_bits = total_bits if total_bits is not None else int(info.total_bits)
         import torch
         self.device = torch.device("cuda", torch.cuda.current_device())
@@ -195,11 +196,21 @@ class DeviceStream:
                   _lib.ptr(payload), payload.size, _lib.ptr(index), index.size, ctypes.byref(h))
         return cls(h, stream.mode, total_bits=int(stream.total_bits))
 
+    def relayout(self, layout="skeleton-first"):
+        """Permute the device payload in place (whff_dstream_relayout): same
+        bytes and index, decodes to the same words; to_host() restores the
+        reference bytes."""
+        _lib.call("whff_dstream_relayout", self._h, _lib.LAYOUT[layout], _lib.cur_stream())
+        self.layout = layout
+        return self
+
     def clone(self):
         """A physically distinct HBM copy (whff_dstream_clone)."""
         h = ctypes.c_void_p()
         _lib.call("whff_dstream_clone", self._h, ctypes.byref(h))
-        return DeviceStream(h, self.mode, total_bits=self.total_bits)
+        c = DeviceStream(h, self.mode, total_bits=self.total_bits)
+        c.layout = self.layout
+        return c
 
     def to_host(self):
         payload = np.empty(self.payload_bytes, dtype=np.uint8)
@@ -267,10 +278,11 @@ class DeviceStream:
         return out
 
 
-def to_device(stream, device=None):
-    if isinstance(stream, DeviceStream):
-        return stream
-    return DeviceStream.from_host(stream, device)
+def to_device(stream, device=None, layout="reference"):
+    ds = stream if isinstance(stream, DeviceStream) else DeviceStream.from_host(stream, device)
+    if layout != ds.layout:
+        ds.relayout(layout)
+    return ds
 
 
 # ---------------------------------------------------------------------------

@@ -24,6 +24,7 @@
 #include "../../include/whff_b200.h"
 #include "whff_decode.cuh"
 #include "whff_encode.cuh"
+#include "whff_relayout.cuh"
 
 using namespace whff;
 
@@ -68,6 +69,7 @@ struct StreamView {
   int32_t kind;
   int32_t planes_limit;
   int32_t has_raw;
+  int32_t layout;
 };
 
 struct whff_dstream {
@@ -77,6 +79,7 @@ struct whff_dstream {
   uint64_t rows, cols, br, bc, nb, gpr;
   uint64_t payload_bytes, payload_bits, total_bits = 0;
   int planes_limit, has_raw, kind;
+  int layout = WHFF_LAYOUT_REFERENCE;
   uint32_t seg_bits;
   uint8_t* d_payload = nullptr;
   size_t payload_alloc = 0;
@@ -101,6 +104,7 @@ struct whff_dstream {
     v.kind = kind;
     v.planes_limit = planes_limit;
     v.has_raw = has_raw;
+    v.layout = layout;
     return v;
   }
 };
@@ -131,6 +135,16 @@ __device__ void block_extent(const StreamView& s, uint64_t b, uint64_t& start, i
   }
 }
 
+// either layout, refill path, for the thread-per-block kernels
+template <bool HAS_RAW>
+__device__ __forceinline__ void decode_any(const StreamView& s, BitWin& bw, int planes_limit,
+                                           Decoded& d) {
+  if (s.layout == WHFF_LAYOUT_SKELETON_FIRST)
+    decode_block_sf<HAS_RAW, true>(bw, planes_limit, d);
+  else
+    decode_block<HAS_RAW, true>(bw, planes_limit, d, __activemask());
+}
+
 // ---------------------------------------------------------------------------
 // decode_blocks parity hook (K:371-408)
 // ---------------------------------------------------------------------------
@@ -148,7 +162,7 @@ __global__ void __launch_bounds__(128) k_decode_blocks(StreamView s, uint64_t fi
   BitWin bw;
   win_at(bw, s.words, start, len);
   Decoded d;
-  decode_block<HAS_RAW, true>(bw, planes_limit, d, __activemask());
+  decode_any<HAS_RAW>(s, bw, planes_limit, d);
   emax[i] = (uint16_t)d.emax;
   raw[i] = (uint8_t)d.raw;
   consumed[i] = (uint64_t)d.consumed;
@@ -174,7 +188,7 @@ __global__ void __launch_bounds__(128) k_decode_block_words(StreamView s, uint64
   BitWin bw;
   win_at(bw, s.words, start, len);
   Decoded d;
-  decode_block<HAS_RAW, true>(bw, s.planes_limit, d, __activemask());
+  decode_any<HAS_RAW>(s, bw, s.planes_limit, d);
   float x[16];
   reconstruct_words(d, x);
 #pragma unroll
@@ -195,7 +209,7 @@ __global__ void __launch_bounds__(128) k_decode_words(StreamView s, float* out, 
   BitWin bw;
   win_at(bw, s.words, start, len);
   Decoded d;
-  decode_block<HAS_RAW, true>(bw, s.planes_limit, d, __activemask());
+  decode_any<HAS_RAW>(s, bw, s.planes_limit, d);
   float x[16];
   reconstruct_words(d, x);
   const uint64_t r0 = (b / s.bc) * 4, c0 = (b % s.bc) * 4;
@@ -335,7 +349,7 @@ constexpr int kGemvWarps = 8;
 #define WHFF_GEMV_LB __launch_bounds__(256)
 #endif
 
-template <int VAR, int EVAL>
+template <int VAR, int EVAL, bool SF>
 __global__ void WHFF_GEMV_LB k_decode_gemv(JobTable T, int policy,
                                                      unsigned long long* status) {
   using TR = VarTraits<VAR>;
@@ -394,7 +408,8 @@ __global__ void WHFF_GEMV_LB k_decode_gemv(JobTable T, int policy,
       const uint64_t bn = bcol + 32 * kGemvWarps;
       if (bn < bc) nxt = ldg(seg128 + row_block0 + bn);   // prefetch this warp's next group
       win_128(bw, q.x, q.y, q.z, q.w, active ? clamp_len(b * 128ull, 128ull, s.payload_bits) : 0);
-      decode_block<false, false, false>(bw, pl, d, 0xFFFFFFFFu);
+      if (SF) decode_block_sf<false, false>(bw, pl, d);
+      else decode_block<false, false, false>(bw, pl, d, 0xFFFFFFFFu);
     } else {
       uint64_t start = 0;
       int len = 0;
@@ -424,10 +439,13 @@ __global__ void WHFF_GEMV_LB k_decode_gemv(JobTable T, int policy,
         bw.avail = 128;
         bw.src = s.words;
       }
-      if (__any_sync(0xFFFFFFFFu, active && !fits_no_refill(start, len)))
-        decode_block<TR::kRaw, true>(bw, pl, d, 0xFFFFFFFFu);
-      else
-        decode_block<TR::kRaw, false>(bw, pl, d, 0xFFFFFFFFu);
+      if (__any_sync(0xFFFFFFFFu, active && !fits_no_refill(start, len))) {
+        if (SF) decode_block_sf<TR::kRaw, true>(bw, pl, d);
+        else decode_block<TR::kRaw, true>(bw, pl, d, 0xFFFFFFFFu);
+      } else {
+        if (SF) decode_block_sf<TR::kRaw, false>(bw, pl, d);
+        else decode_block<TR::kRaw, false>(bw, pl, d, 0xFFFFFFFFu);
+      }
     }
     if (!active) continue;
     const uint32_t colmask = (bcol + 1 == bc) ? last_colmask : 0xFu;
@@ -703,6 +721,20 @@ __global__ void k_source_term(const float* fp, const float* dark, float dose, ui
   const uint64_t i = blockIdx.x * (uint64_t)blockDim.x + threadIdx.x;
   if (i >= n) return;
   u[i] = fp ? __fadd_rn(__fmul_rn(dose, fp[i]), dark[i]) : dark[i];
+}
+
+// ---------------------------------------------------------------------------
+// skeleton-first layout (whff_relayout.cuh): per-block permutation
+// ---------------------------------------------------------------------------
+__global__ void __launch_bounds__(128) k_relayout(StreamView s, const uint32_t* in, uint32_t* out,
+                                                  int inverse) {
+  const uint64_t b = blockIdx.x * (uint64_t)blockDim.x + threadIdx.x;
+  if (b >= s.br * s.bc) return;
+  uint64_t start;
+  int len;
+  block_extent(s, b, start, len);
+  if (inverse) unrelayout_segment(in, out, start, len, s.planes_limit, s.has_raw != 0);
+  else relayout_segment(in, out, start, len, s.planes_limit, s.has_raw != 0);
 }
 
 // ---------------------------------------------------------------------------
@@ -1011,6 +1043,40 @@ whff_status_t whff_dstream_create_segments(int device, const uint8_t* payload, u
   return WHFF_OK;
 }
 
+// permuted copy of the payload (forward: reference -> skeleton-first)
+static whff_status_t permuted_payload(const whff_dstream* s, bool inverse, uint8_t** out,
+                                      cudaStream_t cs) {
+  uint8_t* np = nullptr;
+  cudaError_t e = cudaMalloc(&np, s->payload_alloc);
+  if (e == cudaSuccess) e = cudaMemcpyAsync(np, s->d_payload, s->payload_alloc, cudaMemcpyDeviceToDevice, cs);
+  if (e != cudaSuccess) { cudaFree(np); return cuda_fail(e, "relayout alloc"); }
+  StreamView v = s->view();
+  k_relayout<<<grid_for(s->nb, 128), 128, 0, cs>>>(v, reinterpret_cast<const uint32_t*>(s->d_payload),
+                                                    reinterpret_cast<uint32_t*>(np), inverse ? 1 : 0);
+  e = cudaGetLastError();
+  if (e == cudaSuccess) e = cudaStreamSynchronize(cs);
+  if (e != cudaSuccess) { cudaFree(np); return cuda_fail(e, "relayout"); }
+  *out = np;
+  return WHFF_OK;
+}
+
+whff_status_t whff_dstream_relayout(whff_dstream_t s, int layout, whff_stream_t stream) {
+  if (!s) return fail(WHFF_ERR_ARGUMENT, "null stream");
+  if (layout != WHFF_LAYOUT_REFERENCE && layout != WHFF_LAYOUT_SKELETON_FIRST)
+    return fail(WHFF_ERR_ARGUMENT, "unknown layout");
+  if (layout == s->layout) return WHFF_OK;
+  if (s->kind == WHFF_INDEX_FULL)
+    return fail(WHFF_ERR_ARGUMENT, "relayout needs an implicit or compact index");
+  DeviceGuard g(s->device);
+  uint8_t* np = nullptr;
+  whff_status_t st = permuted_payload(s, layout == WHFF_LAYOUT_REFERENCE, &np, (cudaStream_t)stream);
+  if (st != WHFF_OK) return st;
+  cudaFree(s->d_payload);
+  s->d_payload = np;
+  s->layout = layout;
+  return WHFF_OK;
+}
+
 whff_status_t whff_dstream_clone(whff_dstream_t s, whff_dstream_t* out) {
   if (!s || !out) return fail(WHFF_ERR_ARGUMENT, "null argument");
   *out = nullptr;
@@ -1058,14 +1124,25 @@ whff_status_t whff_dstream_get_info(whff_dstream_t s, whff_dstream_info_t* info)
   info->device_bytes = s->payload_alloc + s->index_bytes;
   info->planes_limit = s->planes_limit;
   info->has_raw_flag = s->has_raw;
+  info->layout = s->layout;
   return WHFF_OK;
 }
 
 whff_status_t whff_dstream_download(whff_dstream_t s, uint8_t* payload, uint64_t* index) {
   if (!s) return fail(WHFF_ERR_ARGUMENT, "null stream");
   DeviceGuard g(s->device);
-  if (payload && s->payload_bytes)
-    WCK(cudaMemcpy(payload, s->d_payload, s->payload_bytes, cudaMemcpyDeviceToHost));
+  if (payload && s->payload_bytes) {
+    if (s->layout == WHFF_LAYOUT_SKELETON_FIRST) {     // restore the reference bytes
+      uint8_t* tmp = nullptr;
+      whff_status_t st = permuted_payload(s, true, &tmp, (cudaStream_t)0);
+      if (st != WHFF_OK) return st;
+      cudaError_t e = cudaMemcpy(payload, tmp, s->payload_bytes, cudaMemcpyDeviceToHost);
+      cudaFree(tmp);
+      if (e != cudaSuccess) return cuda_fail(e, "download payload");
+    } else {
+      WCK(cudaMemcpy(payload, s->d_payload, s->payload_bytes, cudaMemcpyDeviceToHost));
+    }
+  }
   if (index) {
     if (s->kind == WHFF_INDEX_IMPLICIT) {
       for (uint64_t b = 0; b < s->nb; ++b) index[b] = b * s->seg_bits;
@@ -1289,26 +1366,30 @@ static int variant_of(const whff_dstream* s) {
   return s->has_raw ? 3 : 2;
 }
 
-template <int EVAL>
+template <int EVAL, bool SF>
 static whff_status_t launch_gemv_var(int var, const JobTable& T, int policy,
                                      unsigned long long* status, cudaStream_t cs) {
   const unsigned threads = 32 * kGemvWarps;
   const unsigned blocks = (unsigned)T.total_warps;   // one CTA per block-row
   if (blocks == 0) return WHFF_OK;
   switch (var) {
-    case 0: k_decode_gemv<0, EVAL><<<blocks, threads, 0, cs>>>(T, policy, status); break;
-    case 1: k_decode_gemv<1, EVAL><<<blocks, threads, 0, cs>>>(T, policy, status); break;
-    case 2: k_decode_gemv<2, EVAL><<<blocks, threads, 0, cs>>>(T, policy, status); break;
-    default: k_decode_gemv<3, EVAL><<<blocks, threads, 0, cs>>>(T, policy, status); break;
+    case 0: k_decode_gemv<0, EVAL, SF><<<blocks, threads, 0, cs>>>(T, policy, status); break;
+    case 1: k_decode_gemv<1, EVAL, SF><<<blocks, threads, 0, cs>>>(T, policy, status); break;
+    case 2: k_decode_gemv<2, EVAL, SF><<<blocks, threads, 0, cs>>>(T, policy, status); break;
+    default: k_decode_gemv<3, EVAL, SF><<<blocks, threads, 0, cs>>>(T, policy, status); break;
   }
   WCK_LAUNCH("decode_gemv");
   return WHFF_OK;
 }
 
-static whff_status_t launch_gemv(int var, int eval, const JobTable& T, int policy,
+static whff_status_t launch_gemv(int var, int eval, bool sf, const JobTable& T, int policy,
                                  unsigned long long* status, cudaStream_t cs) {
-  if (eval == WHFF_EVAL_COEFF) return launch_gemv_var<WHFF_EVAL_COEFF>(var, T, policy, status, cs);
-  return launch_gemv_var<WHFF_EVAL_EXACT>(var, T, policy, status, cs);
+  if (sf) {
+    if (eval == WHFF_EVAL_COEFF) return launch_gemv_var<WHFF_EVAL_COEFF, true>(var, T, policy, status, cs);
+    return launch_gemv_var<WHFF_EVAL_EXACT, true>(var, T, policy, status, cs);
+  }
+  if (eval == WHFF_EVAL_COEFF) return launch_gemv_var<WHFF_EVAL_COEFF, false>(var, T, policy, status, cs);
+  return launch_gemv_var<WHFF_EVAL_EXACT, false>(var, T, policy, status, cs);
 }
 
 extern "C" whff_status_t whff_decode_gemv_workspace_size(whff_dstream_t s, int eval, size_t* bytes) {
@@ -1354,13 +1435,15 @@ extern "C" whff_status_t whff_decode_gemv(whff_dstream_t s, const float* v, floa
     WCK_LAUNCH("coeff_prep");
     T.single.U = reinterpret_cast<const float4*>(ws);
   }
-  return launch_gemv(variant_of(s), eval, T, policy, reinterpret_cast<unsigned long long*>(status), cs);
+  return launch_gemv(variant_of(s), eval, s->layout == WHFF_LAYOUT_SKELETON_FIRST, T, policy,
+                     reinterpret_cast<unsigned long long*>(status), cs);
 }
 
 struct whff_gemv_plan {
   int device = 0;
   int n = 0;
   int policy = 0, eval = 0, var = 0;
+  bool sf = false;
   GemvJob* d_jobs = nullptr;
   uint64_t* d_prefix = nullptr;
   uint64_t total_warps = 0;
@@ -1382,8 +1465,9 @@ whff_status_t whff_gemv_plan_create(int n, const whff_dstream_t* streams, const 
   if (st != WHFF_OK) return st;
   const int var = variant_of(streams[0]);
   for (int i = 0; i < n; ++i) {
-    if (!streams[i] || variant_of(streams[i]) != var || streams[i]->mode != streams[0]->mode)
-      return fail(WHFF_ERR_ARGUMENT, "plan streams must share mode and index kind");
+    if (!streams[i] || variant_of(streams[i]) != var || streams[i]->mode != streams[0]->mode ||
+        streams[i]->layout != streams[0]->layout)
+      return fail(WHFF_ERR_ARGUMENT, "plan streams must share mode, index kind and layout");
     if (rb[i] > re[i] || re[i] > streams[i]->rows) return fail(WHFF_ERR_DIMENSION, "bad row range");
   }
   whff_gemv_plan* P = new whff_gemv_plan();
@@ -1392,6 +1476,7 @@ whff_status_t whff_gemv_plan_create(int n, const whff_dstream_t* streams, const 
   P->policy = policy;
   P->eval = eval;
   P->var = var;
+  P->sf = streams[0]->layout == WHFF_LAYOUT_SKELETON_FIRST;
   std::vector<GemvJob> jobs(n);
   std::vector<uint64_t> prefix(n), uoff(n, 0);
   uint64_t warps = 0, ucount = 0;
@@ -1469,7 +1554,7 @@ whff_status_t whff_gemv_plan_launch(whff_gemv_plan_t P, uint64_t* status, whff_s
   T.n = P->n;
   T.total_warps = P->total_warps;
   memset(&T.single, 0, sizeof(T.single));
-  return launch_gemv(P->var, P->eval, T, P->policy, reinterpret_cast<unsigned long long*>(status), cs);
+  return launch_gemv(P->var, P->eval, P->sf, T, P->policy, reinterpret_cast<unsigned long long*>(status), cs);
 }
 
 whff_status_t whff_gemv_plan_traffic(whff_gemv_plan_t P, uint64_t* br, uint64_t* bw, uint64_t* nb) {

@@ -1,0 +1,482 @@
+// whff_relayout.cuh -- skeleton-first device layout of WHFZ blocks.
+//
+// The reference bitstream (K:139-225 / K:286-368) interleaves, plane by plane,
+// the refinement bits of the significant coefficients with the significance
+// pass ("skeleton": group flags, insignificant runs, hits, signs).  Decoding
+// it on a SIMT machine costs ~2,000 instructions per block because every
+// plane must be walked and refinement bits arrive in rank order (see
+// whff_decode.cuh).  The skeleton-first layout is a lossless PERMUTATION of
+// each block's segment, computed on the device at upload:
+//
+//     [header][skeleton bits, read order][refinement bits of coefficient 0,
+//      plane order][... of coefficient 1]...[... of coefficient 15][tail]
+//
+// where "read order" and "tail" (the bits the reference decoder never reads)
+// are defined by the reference parse itself.  Segment lengths, offsets, the
+// index and the byte count are unchanged; the inverse permutation restores the
+// reference bytes exactly (tests/test_relayout_host.py round-trips them).
+//
+// The decoder for this layout (decode_block_sf) reproduces the reference's
+// outputs bit-exactly: it walks only the skeleton -- a run of quiet planes is
+// a run of zero flag bits, skipped with one clz and budget arithmetic -- and
+// then reads each coefficient's magnitude as one contiguous field.  No rank
+// insertion, no PDEP and no bit-matrix transpose remain.
+#pragma once
+#include <stdint.h>
+#include "whff_decode.cuh"
+
+namespace whff {
+
+// ---------------------------------------------------------------------------
+// bit-serial exact parse that records the role of every bit read
+// ---------------------------------------------------------------------------
+struct RoleSink {
+  uint32_t skel[48];     // skeleton bits, MSB-first
+  int ns = 0;
+  uint32_t ref[16];      // refinement bits per coefficient, MSB-first (<= 27 bits)
+  int nref[16];
+  WHFF_HD RoleSink() {
+    for (int i = 0; i < 48; ++i) skel[i] = 0;
+    for (int c = 0; c < 16; ++c) { ref[c] = 0; nref[c] = 0; }
+  }
+  WHFF_HD void skel_bit(uint32_t b) {
+    if (b) skel[ns >> 5] |= 0x80000000u >> (ns & 31);
+    ++ns;
+  }
+  WHFF_HD void ref_bit(int c, uint32_t b) {
+    ref[c] = (ref[c] << 1) | b;
+    ++nref[c];
+  }
+};
+
+// single-bit reader over a segment (positions relative to its start)
+struct SegBits {
+  const uint32_t* words;  // LE payload words
+  uint64_t start;
+  int len;
+  WHFF_HD uint32_t get(int pos) const {
+    const uint64_t a = start + (uint64_t)pos;
+    return (bswap32(ldg(words + (a >> 5))) >> (31 - (a & 31))) & 1u;
+  }
+};
+
+// K:286-368 with role recording.  Returns the bits consumed and whether the
+// block has a permutable plane section (not raw / zero / truncated header).
+WHFF_HD int parse_roles(const SegBits& in, int planes_limit, bool has_raw, RoleSink& rs,
+                        int& hdr_bits, bool& permutable) {
+  int pos = 0;
+  const int limit = in.len;
+  permutable = false;
+  hdr_bits = 0;
+  int code = 0;
+  for (int i = 0; i < 9; ++i) {
+    if (pos >= limit) return pos;
+    code = (code << 1) | (int)in.get(pos++);
+  }
+  if (has_raw) {
+    if (pos >= limit) return pos;
+    if (in.get(pos++)) {                     // raw escape: 16 verbatim words
+      const int end = pos + 512;
+      return end < limit ? end : limit;
+    }
+  }
+  if (code == 0) return pos;
+  hdr_bits = pos;
+  permutable = true;
+  uint32_t sig = 0;
+  const int pl = planes_limit < kNPlanes ? planes_limit : kNPlanes;
+  for (int t = 0; t < pl; ++t) {
+    const int p = 26 - t;
+    (void)p;
+    if (pos >= limit) break;
+    for (int c = 0; c < 16; ++c) {           // refinement pass
+      if ((sig >> c) & 1u) {
+        if (pos >= limit) return pos;
+        rs.ref_bit(c, in.get(pos++));
+      }
+    }
+    uint32_t rem = ~sig & 0xFFFFu;           // significance pass
+    while (rem) {
+      if (pos >= limit) return pos;
+      const uint32_t flag = in.get(pos++);
+      rs.skel_bit(flag);
+      if (!flag) break;
+      bool hit = false;
+      for (uint32_t r = rem; r; r &= r - 1) {
+        const uint32_t h = r & (0u - r);
+        if (pos >= limit) return pos;
+        const uint32_t v = in.get(pos++);
+        rs.skel_bit(v);
+        if (v) {
+          if (pos >= limit) return pos;      // sign unavailable
+          rs.skel_bit(in.get(pos++));
+          sig |= h;
+          rem = r & ~(h | (h - 1));
+          hit = true;
+          break;
+        }
+      }
+      if (!hit) break;
+    }
+  }
+  return pos;
+}
+
+// bit writer into a local word buffer (MSB-first)
+WHFF_HD void put_bits(uint32_t* o, int& at, uint32_t v, int n) {  // n <= 32, v in low n bits
+  if (n <= 0) return;
+  v = n == 32 ? v : (v & ((1u << n) - 1u));
+  const int w = at >> 5, off = at & 31;
+  const int room = 32 - off;
+  if (n <= room) {
+    o[w] |= v << (room - n);
+  } else {
+    o[w] |= v >> (n - room);
+    o[w + 1] |= v << (32 - (n - room));
+  }
+  at += n;
+}
+
+// Replace segment bits [0, nbits) of the output payload with the first nbits
+// of `o` (MSB-first).  Neighbouring blocks share boundary words, so the
+// update is two atomic bitwise ops on disjoint bits.
+WHFF_HD void store_bits(uint32_t* out_words, uint64_t start, const uint32_t* o, int nbits) {
+  for (int i = 0; i < nbits;) {
+    const uint64_t a = start + (uint64_t)i;
+    const int off = (int)(a & 31);
+    const int take = (32 - off) < (nbits - i) ? (32 - off) : (nbits - i);
+    // bits [i, i+take) of o, aligned to word offset `off`
+    const int w = i >> 5, s = i & 31;
+    uint32_t chunk = (o[w] << s) | (s ? (o[w + 1] >> (32 - s)) : 0u);   // o bits from i, MSB-first
+    chunk = take == 32 ? chunk : (chunk & ~(0xFFFFFFFFu >> take));      // keep `take` bits
+    const uint32_t be = chunk >> off;                                   // into word position
+    const uint32_t mask = (take == 32 ? 0xFFFFFFFFu : ~(0xFFFFFFFFu >> take)) >> off;
+    uint32_t* dst = out_words + (a >> 5);
+#if defined(__CUDA_ARCH__)
+    atomicAnd(dst, ~bswap32(mask));
+    atomicOr(dst, bswap32(be));
+#else
+    *dst = (*dst & ~bswap32(mask)) | bswap32(be);
+#endif
+    i += take;
+  }
+}
+
+// Forward permutation of one block segment (out_words must hold a copy of the
+// input payload: the tail and any gaps stay as they are).
+WHFF_HD void relayout_segment(const uint32_t* in_words, uint32_t* out_words, uint64_t start,
+                              int len, int planes_limit, bool has_raw) {
+  SegBits in{in_words, start, len};
+  RoleSink rs;
+  int hdr = 0;
+  bool perm = false;
+  const int consumed = parse_roles(in, planes_limit, has_raw, rs, hdr, perm);
+  if (!perm) return;                         // raw / zero / truncated: verbatim
+  uint32_t o[48];
+  for (int i = 0; i < 48; ++i) o[i] = 0;
+  int at = 0;
+  for (int i = 0; i < hdr; ++i) put_bits(o, at, in.get(i), 1);
+  for (int i = 0; i < rs.ns; ++i) put_bits(o, at, (rs.skel[i >> 5] >> (31 - (i & 31))) & 1u, 1);
+  for (int c = 0; c < 16; ++c) put_bits(o, at, rs.ref[c], rs.nref[c]);
+  (void)consumed;
+  store_bits(out_words, start, o, at);
+}
+
+// ---------------------------------------------------------------------------
+// Skeleton-first decoder
+// ---------------------------------------------------------------------------
+// Skeleton walk with the reference's bit budget B (= segment bits after the
+// header): refinement of plane P costs n bits, its significance pass costs
+// the skeleton bits it reads.  Runs of quiet planes (flag 0) are skipped in
+// bulk.  Outputs per coefficient the plane at which it became significant
+// (psig, local memory), and (p_last, cut, sig_last): the last plane whose
+// refinement was read, how many of its ranks got a bit, and the significant
+// set at that refinement.
+template <bool REFILL>
+struct SkelWalk {
+  BitWin& bw;
+  uint8_t* psig;
+  uint32_t sig = 0, negm = 0;
+  int n = 0;
+  int B = 0;
+  int t = 0;           // current plane index from the top (P = 26 - t)
+  int p_last = 26, cut = 0;
+  uint32_t sig_last = 0;
+  bool ended = false;
+  WHFF_HD SkelWalk(BitWin& b, uint8_t* ps) : bw(b), psig(ps) {}
+
+  // refinement of the plane at index t
+  WHFF_HD void refine() {
+    p_last = 26 - t;
+    sig_last = sig;
+    if (B < n) { cut = B; B = 0; ended = true; return; }
+    B -= n;
+    cut = n;
+  }
+  // advance to the next plane (and read its refinement) or end
+  WHFF_HD void next_plane(int pl) {
+    if (t + 1 >= pl) { ended = true; return; }
+    ++t;
+    refine();
+  }
+
+  WHFF_HD void run(int pl) {
+    t = 0;
+    refine();                                // plane 26: n = 0
+    while (!ended) {
+      const int krem0 = 16 - n;
+      if (krem0 == 0) {                      // all significant: no flags remain
+        next_plane(pl);
+        continue;
+      }
+      // bulk: m quiet planes = m zero flags + (m) next refinements of n bits
+      {
+        const int zf = (int)clz32(bw.w0);
+        int m = zf;
+        const int planes_left = pl - 1 - t;
+        if (m > planes_left) m = planes_left;
+        const int mb = B / (n + 1);
+        if (m > mb) m = mb;
+        if (m > 0) {
+          adv<REFILL>(bw, (uint32_t)m);
+          B -= m * (n + 1);
+          t += m;
+          p_last = 26 - t;
+          sig_last = sig;
+          cut = n;
+          continue;
+        }
+      }
+      // one plane's flag at the boundary of budget / planes / window
+      if (B == 0) { ended = true; break; }
+      const uint32_t flag = bw.w0 >> 31;
+      adv<REFILL>(bw, 1);
+      B -= 1;
+      if (!flag) { next_plane(pl); continue; }
+      events(pl);
+    }
+  }
+
+  // significance events of plane P = 26 - t after a raised flag
+  WHFF_HD void events(int pl) {
+    const int P = 26 - t;
+    uint32_t rem = ~sig & 0xFFFFu;
+    int krem = 16 - n;
+    while (true) {
+      const uint32_t y = bw.w0;
+      const int z = (int)clz32(y);
+      if (z >= krem) {                       // no hit: krem zeros
+        if (B < krem) {                      // the reference read B of them
+          adv<REFILL>(bw, (uint32_t)B);
+          B = 0;
+          ended = true;
+          return;
+        }
+        adv<REFILL>(bw, (uint32_t)krem);
+        B -= krem;
+        break;
+      }
+      if (B < z + 1) {                       // run or hit past the budget:
+        adv<REFILL>(bw, (uint32_t)B);        // B zeros of the run were read
+        B = 0;
+        ended = true;
+        return;
+      }
+      if (B == z + 1) {                          // sign unavailable (K:353-354)
+        adv<REFILL>(bw, (uint32_t)(z + 1));
+        B = 0;
+        ended = true;
+        return;
+      }
+      const uint32_t sgn = (y << (z + 1)) >> 31;
+      adv<REFILL>(bw, (uint32_t)(z + 2));
+      B -= z + 2;
+      if (z > 0) rem &= rem - 1;
+      if (z > 1) rem &= rem - 1;
+      if (z > 2) rem &= rem - 1;
+      if (z > 3) {
+        rem &= rem - 1;
+        for (int i = 4; i < z; ++i) rem &= rem - 1;
+      }
+      const uint32_t h = rem & (0u - rem);
+      rem ^= h;
+      krem -= z + 1;
+      psig[31 - clz32(h)] = (uint8_t)P;
+      sig |= h;
+      if (sgn) negm |= h;
+      n += 1;
+      if (krem == 0) break;
+      if (B == 0) { ended = true; return; }
+      const uint32_t f = bw.w0 >> 31;
+      adv<REFILL>(bw, 1);
+      B -= 1;
+      if (!f) break;
+    }
+    next_plane(pl);
+  }
+};
+
+template <bool HAS_RAW, bool REFILL>
+WHFF_HD void decode_block_sf(BitWin& bw, int planes_limit, Decoded& d) {
+  const int len = bw.len;
+  d.negm = 0;
+  d.emax = 0;
+  d.raw = 0;
+#pragma unroll
+  for (int c = 0; c < 16; ++c) d.mag[c] = 0;
+  if (len < 9) { d.consumed = len < 0 ? 0 : len; return; }
+  const uint32_t hdr = bw.w0;
+  const uint32_t code = hdr >> 23;
+  d.emax = code;
+  int hbits = 9;
+  if (HAS_RAW) {
+    if (len < 10) { d.consumed = 9; return; }
+    if ((hdr >> 22) & 1u) {                  // raw escape: same as WHFZ
+      adv<REFILL>(bw, 10);
+      d.raw = 1;
+      int nw = (len - 10) >> 5;
+      if (nw > 16) nw = 16;
+#pragma unroll
+      for (int c = 0; c < 16; ++c) {
+        if (c < nw) {
+          d.mag[c] = bw.w0;
+          adv<REFILL>(bw, 32);
+        }
+      }
+      d.consumed = (len - 10 >= 512) ? 522 : len;
+      return;
+    }
+    hbits = 10;
+  }
+  adv<REFILL>(bw, (uint32_t)hbits);
+  if (code == 0) { d.consumed = hbits; return; }
+
+  const int pl = planes_limit < kNPlanes ? planes_limit : kNPlanes;
+  if (pl <= 0) { d.consumed = hbits; return; }
+  uint8_t psig[16];
+  SkelWalk<REFILL> w(bw, psig);
+  w.B = len - hbits;
+  w.run(pl);
+  d.negm = w.negm;
+  // coefficient-major refinement fields, index order (K:326-332 bits)
+  const uint32_t sig = w.sig, sig_last = w.sig_last;
+  const int p_last = w.p_last, cut = w.cut;
+#pragma unroll
+  for (int c = 0; c < 16; ++c) {
+    if ((sig >> c) & 1u) {
+      const int ps = psig[c];
+      int l = ps - 1 - p_last;
+      l = l < 0 ? 0 : l;
+      if ((sig_last >> c) & 1u) {
+        const int rank = (int)popc32(sig_last & ((1u << c) - 1u));
+        l += rank < cut ? 1 : 0;
+      }
+      const uint32_t field = l ? (bw.w0 >> (32 - l)) : 0u;
+      adv<REFILL>(bw, (uint32_t)l);
+      d.mag[c] = (1u << ps) | (field << (ps - l));
+    }
+  }
+  d.consumed = bw.pos;
+}
+
+// ---------------------------------------------------------------------------
+// Inverse permutation (skeleton-first -> reference bytes)
+// ---------------------------------------------------------------------------
+// Pass 1 walks the skeleton to learn every coefficient's refinement length;
+// pass 2 replays the reference's read order, drawing skeleton bits and each
+// coefficient's refinement bits from their regions.
+WHFF_HD void unrelayout_segment(const uint32_t* in_words, uint32_t* out_words, uint64_t start,
+                                int len, int planes_limit, bool has_raw) {
+  SegBits in{in_words, start, len};
+  if (len < 9) return;
+  int code = 0;
+  for (int i = 0; i < 9; ++i) code = (code << 1) | (int)in.get(i);
+  int hbits = 9;
+  if (has_raw) {
+    if (len < 10) return;
+    if (in.get(9)) return;                   // raw: verbatim
+    hbits = 10;
+  }
+  if (code == 0) return;
+  // pass 1: the decoder's skeleton walk on the permuted segment
+  BitWin bw;
+  win_at(bw, in_words, start, len);
+  adv<true>(bw, (uint32_t)hbits);
+  const int pl = planes_limit < kNPlanes ? planes_limit : kNPlanes;
+  if (pl <= 0) return;
+  uint8_t psig[16];
+  SkelWalk<true> w(bw, psig);
+  w.B = len - hbits;
+  w.run(pl);
+  const int skel_end = bw.pos;                // end of the skeleton region
+  int rstart[16], rlen[16];
+  int at = skel_end;
+  for (int c = 0; c < 16; ++c) {
+    int l = 0;
+    if ((w.sig >> c) & 1u) {
+      l = psig[c] - 1 - w.p_last;
+      l = l < 0 ? 0 : l;
+      if ((w.sig_last >> c) & 1u) {
+        const int rank = (int)popc32(w.sig_last & ((1u << c) - 1u));
+        l += rank < w.cut ? 1 : 0;
+      }
+    }
+    rstart[c] = at;
+    rlen[c] = l;
+    at += l;
+  }
+  // pass 2: replay K:286-368 order
+  uint32_t o[48];
+  for (int i = 0; i < 48; ++i) o[i] = 0;
+  int wr = 0;
+  for (int i = 0; i < hbits; ++i) put_bits(o, wr, in.get(i), 1);
+  int sk = hbits;                             // skeleton cursor
+  int rc[16];
+  for (int c = 0; c < 16; ++c) rc[c] = 0;
+  int pos = hbits;                            // reference read position
+  const int limit = len;
+  uint32_t sig = 0;
+  bool stop = false;
+  for (int t = 0; t < pl && !stop; ++t) {
+    if (pos >= limit) break;
+    for (int c = 0; c < 16 && !stop; ++c) {
+      if ((sig >> c) & 1u) {
+        if (pos >= limit) { stop = true; break; }
+        const uint32_t b = rc[c] < rlen[c] ? in.get(rstart[c] + rc[c]) : 0u;
+        ++rc[c];
+        put_bits(o, wr, b, 1);
+        ++pos;
+      }
+    }
+    if (stop) break;
+    uint32_t rem = ~sig & 0xFFFFu;
+    while (rem && !stop) {
+      if (pos >= limit) { stop = true; break; }
+      const uint32_t flag = in.get(sk++);
+      put_bits(o, wr, flag, 1);
+      ++pos;
+      if (!flag) break;
+      bool hit = false;
+      for (uint32_t r = rem; r; r &= r - 1) {
+        const uint32_t h = r & (0u - r);
+        if (pos >= limit) { stop = true; break; }
+        const uint32_t v = in.get(sk++);
+        put_bits(o, wr, v, 1);
+        ++pos;
+        if (v) {
+          if (pos >= limit) { stop = true; break; }
+          put_bits(o, wr, in.get(sk++), 1);
+          ++pos;
+          sig |= h;
+          rem = r & ~(h | (h - 1));
+          hit = true;
+          break;
+        }
+      }
+      if (!hit) break;
+    }
+  }
+  store_bits(out_words, start, o, wr);
+}
+
+}  // namespace whff

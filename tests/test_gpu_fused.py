@@ -151,3 +151,30 @@ def test_fused_checksum_property_mid_size(rng):
     assert (np.abs(y - y2) <= 2 * b).all()
     colsum = Cn.astype(np.float64).sum(0)
     assert abs(y.sum() - colsum @ v.cpu().numpy().astype(np.float64)) <= 1e-6 * np.abs(y).sum()
+
+
+@pytest.mark.parametrize("mode_kind,param", [("rate", 8), ("rate", 3), ("precision", 17),
+                                             ("accuracy", 1e-12), ("accuracy", 0.0)])
+def test_skeleton_first_layout_identical(orc, mode_kind, param, rng):
+    """whff_dstream_relayout: same decoded words, same decode_blocks arrays,
+    bit-identical fused products, reference bytes restored on download."""
+    import torch
+    from paper_1902_08018_b200 import codec
+    mode = {"rate": codec.FixedRate, "precision": codec.FixedPrecision,
+            "accuracy": codec.FixedAccuracy}[mode_kind](param)
+    C0 = smooth_matrix(130, 3000) if param != 0.0 else rng.standard_normal((37, 91)).astype(np.float32)
+    host = codec.compress(C0, mode)
+    ref = codec.DeviceStream.from_host(host)
+    sf = codec.DeviceStream.from_host(host).relayout("skeleton-first")
+    assert sf.layout == "skeleton-first"
+    assert torch.equal(ref.decode(), sf.decode())
+    for a, b in zip(ref.decode_blocks(), sf.decode_blocks()):
+        assert torch.equal(a, b)
+    v = torch.from_numpy(rng.random(C0.shape[1]).astype(np.float32)).cuda()
+    for ev in ("exact", "coefficient"):
+        assert torch.equal(ref.gemv(v, evaluation=ev), sf.gemv(v, evaluation=ev))
+    back = sf.to_host()
+    assert np.array_equal(back.payload, host.payload)
+    assert np.array_equal(back.block_index, host.block_index)
+    sf.relayout("reference")
+    assert torch.equal(ref.decode(), sf.decode())

@@ -139,3 +139,51 @@ int64_t hc_encode_blocks(const uint32_t* mag, const uint8_t* neg, const uint16_t
   return (int64_t)total;
 }
 }
+
+#include "../paper_1902_08018_b200/csrc/whff_relayout.cuh"
+extern "C" {
+// forward / inverse skeleton-first permutation of every segment (out must
+// start as a copy of in)
+void hc_relayout(const uint32_t* in, uint32_t* out, const uint64_t* offsets, const uint64_t* seglens,
+                 int64_t nb, uint64_t payload_bits, int planes_limit, int has_raw, int inverse) {
+  for (int64_t b = 0; b < nb; ++b) {
+    uint64_t start = offsets[b], limit = start + seglens[b];
+    if (limit > payload_bits) limit = payload_bits;
+    int64_t l = (int64_t)limit - (int64_t)start;
+    int len = l > 65535 ? 65535 : (int)l;
+    if (inverse) whff::unrelayout_segment(in, out, start, len, planes_limit, has_raw != 0);
+    else whff::relayout_segment(in, out, start, len, planes_limit, has_raw != 0);
+  }
+}
+// decode_blocks on a skeleton-first payload
+void hc_decode_blocks_sf(const uint32_t* words, uint64_t payload_bits, const uint64_t* offsets,
+                         const uint64_t* seglens, int64_t nb, int planes_limit, int has_raw,
+                         uint32_t* mag, uint8_t* neg, uint16_t* emax, uint8_t* raw,
+                         uint32_t* raw_words, uint64_t* consumed) {
+  for (int64_t b = 0; b < nb; ++b) {
+    uint64_t start = offsets[b], limit = start + seglens[b];
+    if (limit > payload_bits) limit = payload_bits;
+    int64_t l = (int64_t)limit - (int64_t)start;
+    int len = l > 65535 ? 65535 : (int)l;
+    whff::BitWin bw;
+    whff::win_at(bw, words, start, len);
+    whff::Decoded d;
+    const bool fits = whff::fits_no_refill(start, len);
+    if (has_raw) {
+      if (!fits) whff::decode_block_sf<true, true>(bw, planes_limit, d);
+      else whff::decode_block_sf<true, false>(bw, planes_limit, d);
+    } else {
+      if (!fits) whff::decode_block_sf<false, true>(bw, planes_limit, d);
+      else whff::decode_block_sf<false, false>(bw, planes_limit, d);
+    }
+    emax[b] = (uint16_t)d.emax;
+    raw[b] = (uint8_t)d.raw;
+    consumed[b] = (uint64_t)d.consumed;
+    for (int c = 0; c < 16; ++c) {
+      mag[16 * b + c] = d.raw ? 0u : d.mag[c];
+      raw_words[16 * b + c] = d.raw ? d.mag[c] : 0u;
+      neg[16 * b + c] = (uint8_t)((d.negm >> c) & 1u);
+    }
+  }
+}
+}

@@ -14,6 +14,7 @@ from paper_1902_08018_b200 import _lib  # noqa: E402
 mode_s = sys.argv[1] if len(sys.argv) > 1 else "rate:8"
 ev = sys.argv[2] if len(sys.argv) > 2 else "exact"
 nsl = int(sys.argv[3]) if len(sys.argv) > 3 else 4
+layout = sys.argv[4] if len(sys.argv) > 4 else "reference"
 kind, p = mode_s.split(":")
 mode = {"rate": codec.FixedRate, "precision": codec.FixedPrecision,
         "accuracy": codec.FixedAccuracy}[kind](int(p) if kind != "accuracy" else float(p))
@@ -21,7 +22,10 @@ spec = synth.Spec(grid_rows=608, grid_cols=608, S=256000, K=378 * nsl, M=378, se
 streams = []
 for s in range(nsl):
     rows = synth.deformation_rows(spec, 0, 0.3, s * 378, (s + 1) * 378, device="cuda")
-    streams.append(codec.compress_device(rows, mode))
+    ds = codec.compress_device(rows, mode)
+    if layout != "reference":
+        ds.relayout(layout)
+    streams.append(ds)
 v = torch.rand(256000, device="cuda")
 y = torch.zeros(378 * nsl, device="cuda")
 plan = GemvPlan([(ds, v, y[i * 378:(i + 1) * 378], 0, 378) for i, ds in enumerate(streams)],
@@ -37,5 +41,5 @@ for _ in range(5):
 e1.record()
 torch.cuda.synchronize()
 ms = e0.elapsed_time(e1) / 5
-print(f"{mode_s} {ev} slits={nsl}: {ms:.3f} ms/launch, {plan.bytes_read / ms / 1e6:.1f} GB/s, "
+print(f"{mode_s} {ev} {layout} slits={nsl}: {ms:.3f} ms/launch, {plan.bytes_read / ms / 1e6:.1f} GB/s, "
       f"blocks={plan.n_blocks}")
