@@ -17,8 +17,8 @@ ROOT = os.path.dirname(HERE)
 CSRC = os.path.join(HERE, "csrc")
 LIB = os.path.join(HERE, "libwhff_b200.so")
 SOURCES = [os.path.join(CSRC, "whff_b200.cu")]
-HEADERS = [os.path.join(CSRC, "whff_decode.cuh"), os.path.join(CSRC, "whff_encode.cuh"),
-           os.path.join(ROOT, "include", "whff_b200.h")]
+HEADERS = sorted(os.path.join(CSRC, f) for f in os.listdir(CSRC) if f.endswith((".cuh", ".h"))) + [
+    os.path.join(ROOT, "include", "whff_b200.h")]
 
 NVCC_FLAGS = [
     "-gencode", "arch=compute_100a,code=sm_100a",

@@ -235,8 +235,7 @@ struct SkelWalk {
         int m = zf;
         const int planes_left = pl - 1 - t;
         if (m > planes_left) m = planes_left;
-        const int mb = B / (n + 1);
-        if (m > mb) m = mb;
+        if (m * (n + 1) > B) m = B / (n + 1);    // budget boundary (once per block)
         if (m > 0) {
           adv<REFILL>(bw, (uint32_t)m);
           B -= m * (n + 1);
@@ -289,7 +288,6 @@ struct SkelWalk {
         return;
       }
       const uint32_t sgn = (y << (z + 1)) >> 31;
-      adv<REFILL>(bw, (uint32_t)(z + 2));
       B -= z + 2;
       if (z > 0) rem &= rem - 1;
       if (z > 1) rem &= rem - 1;
@@ -305,10 +303,14 @@ struct SkelWalk {
       sig |= h;
       if (sgn) negm |= h;
       n += 1;
-      if (krem == 0) break;
-      if (B == 0) { ended = true; return; }
-      const uint32_t f = bw.w0 >> 31;
-      adv<REFILL>(bw, 1);
+      if (krem == 0 || B == 0) {             // no further flag (remainder empty / budget)
+        adv<REFILL>(bw, (uint32_t)(z + 2));
+        if (krem != 0) { ended = true; return; }
+        break;
+      }
+      // next group flag sits right after the sign (z + 3 <= 18 bits into y)
+      const uint32_t f = (y << (z + 2)) >> 31;
+      adv<REFILL>(bw, (uint32_t)(z + 3));
       B -= 1;
       if (!f) break;
     }
@@ -361,6 +363,7 @@ WHFF_HD void decode_block_sf(BitWin& bw, int planes_limit, Decoded& d) {
   // coefficient-major refinement fields, index order (K:326-332 bits)
   const uint32_t sig = w.sig, sig_last = w.sig_last;
   const int p_last = w.p_last, cut = w.cut;
+  int rank = 0;                              // running rank within sig_last
 #pragma unroll
   for (int c = 0; c < 16; ++c) {
     if ((sig >> c) & 1u) {
@@ -368,8 +371,8 @@ WHFF_HD void decode_block_sf(BitWin& bw, int planes_limit, Decoded& d) {
       int l = ps - 1 - p_last;
       l = l < 0 ? 0 : l;
       if ((sig_last >> c) & 1u) {
-        const int rank = (int)popc32(sig_last & ((1u << c) - 1u));
         l += rank < cut ? 1 : 0;
+        ++rank;
       }
       const uint32_t field = l ? (bw.w0 >> (32 - l)) : 0u;
       adv<REFILL>(bw, (uint32_t)l);
