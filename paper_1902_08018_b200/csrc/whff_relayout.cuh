@@ -220,10 +220,14 @@ struct SkelWalk {
     refine();
   }
 
+  int iters = 0, hit_iters = 0;             // instrumentation (host statistics)
   WHFF_HD void run(int pl) {
     t = 0;
     refine();                                // plane 26: n = 0
     while (!ended) {
+#if !defined(__CUDA_ARCH__)
+      ++iters;
+#endif
       const int krem0 = 16 - n;
       if (krem0 == 0) {                      // all significant: no flags remain
         next_plane(pl);
@@ -262,6 +266,9 @@ struct SkelWalk {
     uint32_t rem = ~sig & 0xFFFFu;
     int krem = 16 - n;
     while (true) {
+#if !defined(__CUDA_ARCH__)
+      ++hit_iters;
+#endif
       const uint32_t y = bw.w0;
       const int z = (int)clz32(y);
       if (z >= krem) {                       // no hit: krem zeros

@@ -169,11 +169,19 @@ class FieldStep:
             dist.broadcast(self.S, src=0, group=self.group)
         self.products()
 
+    def gather(self):
+        """All-gather the per-rank deformation rows (padded to max_rows)."""
+        import torch.distributed as dist
+        if dist.get_backend(self.group) == "nccl":
+            dist.all_gather_into_tensor(self.gathered, self.local, group=self.group)
+        else:  # gloo (CPU tests, several ranks on one device): list form
+            parts = list(self.gathered.view(self.world, self.max_rows).unbind(0))
+            dist.all_gather(parts, self.local, group=self.group)
+
     def step(self):
         self.step_local()
         if self.world > 1:
-            import torch.distributed as dist
-            dist.all_gather_into_tensor(self.gathered, self.local, group=self.group)
+            self.gather()
 
     def check(self):
         if _lib.read_status(self.status) is not None:

@@ -187,3 +187,28 @@ void hc_decode_blocks_sf(const uint32_t* words, uint64_t payload_bits, const uin
   }
 }
 }
+extern "C" {
+// walk statistics per block (skeleton-first payload): outer / hit iterations
+void hc_walk_stats(const uint32_t* words, uint64_t payload_bits, const uint64_t* offsets,
+                   const uint64_t* seglens, int64_t nb, int planes_limit, int has_raw,
+                   int32_t* outer, int32_t* hits) {
+  for (int64_t b = 0; b < nb; ++b) {
+    uint64_t start = offsets[b], limit = start + seglens[b];
+    if (limit > payload_bits) limit = payload_bits;
+    int len = (int)(limit - start);
+    whff::BitWin bw;
+    whff::win_at(bw, words, start, len);
+    int hb = has_raw ? 10 : 9;
+    uint32_t code = bw.w0 >> 23;
+    outer[b] = hits[b] = 0;
+    if (code == 0 || (has_raw && ((bw.w0 >> 22) & 1u))) continue;
+    whff::adv<true>(bw, hb);
+    uint8_t psig[16];
+    whff::SkelWalk<true> w(bw, psig);
+    w.B = len - hb;
+    w.run(planes_limit);
+    outer[b] = w.iters;
+    hits[b] = w.hit_iters;
+  }
+}
+}
