@@ -192,6 +192,9 @@ WHFF_HD void relayout_segment(const uint32_t* in_words, uint32_t* out_words, uin
 // (psig, local memory), and (p_last, cut, sig_last): the last plane whose
 // refinement was read, how many of its ranks got a bit, and the significant
 // set at that refinement.
+#ifndef WHFF_WALK_FAST
+#define WHFF_WALK_FAST 1
+#endif
 template <bool REFILL>
 struct SkelWalk {
   BitWin& bw;
@@ -202,6 +205,7 @@ struct SkelWalk {
   int t = 0;           // current plane index from the top (P = 26 - t)
   int p_last = 26, cut = 0;
   uint32_t sig_last = 0;
+  uint32_t rem_lo = 0xFFFFu;   // coefficients still eligible in plane t (above its last hit)
   bool ended = false;
   WHFF_HD SkelWalk(BitWin& b, uint8_t* ps) : bw(b), psig(ps) {}
 
@@ -209,6 +213,7 @@ struct SkelWalk {
   WHFF_HD void refine() {
     p_last = 26 - t;
     sig_last = sig;
+    rem_lo = 0xFFFFu;
     if (B < n) { cut = B; B = 0; ended = true; return; }
     B -= n;
     cut = n;
@@ -220,16 +225,97 @@ struct SkelWalk {
     refine();
   }
 
-  int iters = 0, hit_iters = 0;             // instrumentation (host statistics)
+  int iters = 0, hit_iters = 0, fast_iters = 0;   // instrumentation (host statistics)
   WHFF_HD void run(int pl) {
     t = 0;
     refine();                                // plane 26: n = 0
+#if WHFF_WALK_FAST
+    run_fast(pl);
+#endif
+    run_from(pl);
+  }
+
+  // Event loop.  One iteration consumes one token of the skeleton,
+  //   0^m 1 0^z 1 s
+  // = m zero group flags (each ends a plane; the next plane's refinement
+  // costs n bits of budget), a raised flag, z insignificant coefficients of
+  // the remainder, the hit and its sign.  The insignificant coefficients are
+  // kept as an ordered nibble list, so the hit is nibble (off + z) and
+  // removing it is a masked 64-bit merge (no per-coefficient loop).  A token
+  // that would cross the budget, the plane limit or the window, or that has
+  // no hit, leaves the loop untouched; run_from() finishes the block with the
+  // general (reference-order) logic from exactly this state.
+  WHFF_HD void run_fast(int pl) {
+    if (ended) return;
+    uint64_t ins = 0xFEDCBA9876543210ull;    // insignificant coefficients, nibble i = i-th
+    int cnt = 16, off = 0;
+    int lo_c = -1;                           // last hit of plane t (rem_lo), -1 at plane start
+    int tt = t, nn = n, BB = B;
+    uint32_t sg = sig, ng = negm, sl = sig_last;
+    while (true) {
+      const uint32_t x = bw.w0;
+      const int m = (int)clz32(x);
+      const uint32_t y = fsl(x, 0u, (uint32_t)(m + 1 > 32 ? 32 : m + 1));
+      const int z = (int)clz32(y);
+      const int base = m ? 0 : off;
+      const int k = m + z + 3;
+      const int cost = m * (nn + 1) + z + 3;
+      if (z >= cnt - base || k > 32 || tt + m >= pl || cost > BB) break;
+#if !defined(__CUDA_ARCH__)
+      ++fast_iters;
+#endif
+      const uint32_t sgn = (y >> (30 - z)) & 1u;
+      adv<REFILL>(bw, (uint32_t)k);
+      BB -= cost;
+      tt += m;
+      if (m) { sl = sg; lo_c = -1; }
+      const int a = base + z;
+      const uint32_t c = (uint32_t)(ins >> (4 * a)) & 15u;
+      const uint64_t lowm = (1ull << (4 * a)) - 1ull;
+      ins = (ins & lowm) | ((ins >> 4) & ~lowm);
+      cnt -= 1;
+      psig[c] = (uint8_t)(26 - tt);
+      const uint32_t h = 1u << c;
+      sg |= h;
+      ng |= sgn << c;
+      nn += 1;
+      off = a;
+      lo_c = (int)c;
+      if (a == cnt) {                        // remainder empty: the plane ends without a flag
+        if (cnt == 0 || tt + 1 >= pl || nn > BB) break;
+        tt += 1;
+        BB -= nn;
+        sl = sg;
+        off = 0;
+        lo_c = -1;
+      }
+    }
+    t = tt; n = nn; B = BB; sig = sg; negm = ng;
+    sig_last = sl;
+    p_last = 26 - tt;
+    cut = (int)popc32(sl);
+    rem_lo = lo_c < 0 ? 0xFFFFu : (0xFFFFu & ~((2u << lo_c) - 1u));
+  }
+
+  // general walk from any state "refinement of plane t read, next read is a
+  // group flag of plane t (or the plane is exhausted)"
+  WHFF_HD void run_from(int pl) {
     while (!ended) {
 #if !defined(__CUDA_ARCH__)
       ++iters;
 #endif
-      const int krem0 = 16 - n;
-      if (krem0 == 0) {                      // all significant: no flags remain
+      const uint32_t remv = ~sig & rem_lo & 0xFFFFu;
+      if (remv == 0) {                       // remainder empty: no flag, plane ends
+        if (n == 16 && rem_lo == 0xFFFFu) {  // all significant: whole refinement planes
+          int m = pl - 1 - t;
+          if (m * 16 > B) m = B >> 4;
+          if (m > 0) {
+            t += m;
+            B -= m * 16;
+            p_last = 26 - t;
+            cut = 16;
+          }
+        }
         next_plane(pl);
         continue;
       }
@@ -247,6 +333,7 @@ struct SkelWalk {
           p_last = 26 - t;
           sig_last = sig;
           cut = n;
+          rem_lo = 0xFFFFu;
           continue;
         }
       }
@@ -263,8 +350,8 @@ struct SkelWalk {
   // significance events of plane P = 26 - t after a raised flag
   WHFF_HD void events(int pl) {
     const int P = 26 - t;
-    uint32_t rem = ~sig & 0xFFFFu;
-    int krem = 16 - n;
+    uint32_t rem = ~sig & rem_lo & 0xFFFFu;
+    int krem = (int)popc32(rem);
     while (true) {
 #if !defined(__CUDA_ARCH__)
       ++hit_iters;
@@ -296,13 +383,7 @@ struct SkelWalk {
       }
       const uint32_t sgn = (y << (z + 1)) >> 31;
       B -= z + 2;
-      if (z > 0) rem &= rem - 1;
-      if (z > 1) rem &= rem - 1;
-      if (z > 2) rem &= rem - 1;
-      if (z > 3) {
-        rem &= rem - 1;
-        for (int i = 4; i < z; ++i) rem &= rem - 1;
-      }
+      for (int i = 0; i < z; ++i) rem &= rem - 1;
       const uint32_t h = rem & (0u - rem);
       rem ^= h;
       krem -= z + 1;
@@ -310,6 +391,7 @@ struct SkelWalk {
       sig |= h;
       if (sgn) negm |= h;
       n += 1;
+      rem_lo = 0xFFFFu & ~(h | (h - 1u));
       if (krem == 0 || B == 0) {             // no further flag (remainder empty / budget)
         adv<REFILL>(bw, (uint32_t)(z + 2));
         if (krem != 0) { ended = true; return; }

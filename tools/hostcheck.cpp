@@ -208,7 +208,7 @@ void hc_walk_stats(const uint32_t* words, uint64_t payload_bits, const uint64_t*
     w.B = len - hb;
     w.run(planes_limit);
     outer[b] = w.iters;
-    hits[b] = w.hit_iters;
+    hits[b] = w.hit_iters + 1000 * w.fast_iters;
   }
 }
 }
