@@ -249,7 +249,6 @@ struct SkelWalk {
     if (ended) return;
     uint64_t ins = 0xFEDCBA9876543210ull;    // insignificant coefficients, nibble i = i-th
     int cnt = 16, off = 0;
-    int lo_c = -1;                           // last hit of plane t (rem_lo), -1 at plane start
     int tt = t, nn = n, BB = B;
     uint32_t sg = sig, ng = negm, sl = sig_last;
     while (true) {
@@ -268,7 +267,7 @@ struct SkelWalk {
       adv<REFILL>(bw, (uint32_t)k);
       BB -= cost;
       tt += m;
-      if (m) { sl = sg; lo_c = -1; }
+      if (m) sl = sg;
       const int a = base + z;
       const uint32_t c = (uint32_t)(ins >> (4 * a)) & 15u;
       const uint64_t lowm = (1ull << (4 * a)) - 1ull;
@@ -280,21 +279,22 @@ struct SkelWalk {
       ng |= sgn << c;
       nn += 1;
       off = a;
-      lo_c = (int)c;
       if (a == cnt) {                        // remainder empty: the plane ends without a flag
         if (cnt == 0 || tt + 1 >= pl || nn > BB) break;
         tt += 1;
         BB -= nn;
         sl = sg;
         off = 0;
-        lo_c = -1;
       }
     }
     t = tt; n = nn; B = BB; sig = sg; negm = ng;
     sig_last = sl;
     p_last = 26 - tt;
     cut = (int)popc32(sl);
-    rem_lo = lo_c < 0 ? 0xFFFFu : (0xFFFFu & ~((2u << lo_c) - 1u));
+    // eligible remainder of plane t = ins[off:], i.e. every coefficient from
+    // ins[off] up (all lower ones are significant or already skipped)
+    rem_lo = off == 0 ? 0xFFFFu
+           : off >= cnt ? 0u : (0xFFFFu << (uint32_t)((ins >> (4 * off)) & 15u)) & 0xFFFFu;
   }
 
   // general walk from any state "refinement of plane t read, next read is a
@@ -313,6 +313,7 @@ struct SkelWalk {
             t += m;
             B -= m * 16;
             p_last = 26 - t;
+            sig_last = sig;
             cut = 16;
           }
         }
@@ -444,28 +445,42 @@ WHFF_HD void decode_block_sf(BitWin& bw, int planes_limit, Decoded& d) {
 
   const int pl = planes_limit < kNPlanes ? planes_limit : kNPlanes;
   if (pl <= 0) { d.consumed = hbits; return; }
-  uint8_t psig[16];
-  SkelWalk<REFILL> w(bw, psig);
+  alignas(16) uint32_t psw[4] = {0u, 0u, 0u, 0u};   // psig bytes (0 for insignificant)
+  SkelWalk<REFILL> w(bw, reinterpret_cast<uint8_t*>(psw));
   w.B = len - hbits;
   w.run(pl);
   d.negm = w.negm;
-  // coefficient-major refinement fields, index order (K:326-332 bits)
+  // Coefficient-major refinement fields, index order (K:326-332 bits).
+  // Coefficient c, significant at plane ps, holds the bits of planes
+  // ps-1 .. e: e = p_last+1 for the members of sig_last (one lower for the
+  // first `cut` of them, which got plane p_last's bit), e = ps otherwise.
+  // Its magnitude is the leading 1 at bit ps followed by the field:
+  // ((0x80000000 | F >> 1) >> (31 - ps)) with the bits below e cleared.
   const uint32_t sig = w.sig, sig_last = w.sig_last;
-  const int p_last = w.p_last, cut = w.cut;
+  const uint32_t pl1 = (uint32_t)(w.p_last + 1);
+  const int cut = w.cut;
   int rank = 0;                              // running rank within sig_last
+  uint32_t pv[4];
+#if defined(__CUDA_ARCH__)
+  {
+    const uint4 q = *reinterpret_cast<const uint4*>(psw);    // one LDL.128
+    pv[0] = q.x; pv[1] = q.y; pv[2] = q.z; pv[3] = q.w;
+  }
+#else
+  for (int i = 0; i < 4; ++i) pv[i] = psw[i];
+#endif
 #pragma unroll
   for (int c = 0; c < 16; ++c) {
-    if ((sig >> c) & 1u) {
-      const int ps = psig[c];
-      int l = ps - 1 - p_last;
-      l = l < 0 ? 0 : l;
+    if ((sig >> c) & 1u) {                   // skipped when no lane of the warp has it
+      const uint32_t ps = (pv[c >> 2] >> (8 * (c & 3))) & 0xFFu;
+      uint32_t e = ps;
       if ((sig_last >> c) & 1u) {
-        l += rank < cut ? 1 : 0;
+        e = pl1 - (rank < cut ? 1u : 0u);
         ++rank;
       }
-      const uint32_t field = l ? (bw.w0 >> (32 - l)) : 0u;
-      adv<REFILL>(bw, (uint32_t)l);
-      d.mag[c] = (1u << ps) | (field << (ps - l));
+      const uint32_t F = bw.w0;
+      d.mag[c] = (((F >> 1) | 0x80000000u) >> (31u - ps)) & (0xFFFFFFFFu << e);
+      adv<REFILL>(bw, ps - e);
     }
   }
   d.consumed = bw.pos;
