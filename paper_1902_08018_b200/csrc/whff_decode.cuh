@@ -57,6 +57,16 @@ WHFF_HD uint32_t clz32(uint32_t x) {
   return x ? (uint32_t)__builtin_clz(x) : 32u;
 #endif
 }
+// count of leading zeros as one FLO.SH (bfind.shiftamt); 0xFFFFFFFF for x == 0
+WHFF_HD uint32_t clz_sh(uint32_t x) {
+#if defined(__CUDA_ARCH__)
+  uint32_t d;
+  asm("bfind.shiftamt.u32 %0, %1;" : "=r"(d) : "r"(x));
+  return d;
+#else
+  return x ? (uint32_t)__builtin_clz(x) : 0xFFFFFFFFu;
+#endif
+}
 WHFF_HD uint32_t popc32(uint32_t x) {
 #if defined(__CUDA_ARCH__)
   return (uint32_t)__popc(x);

@@ -249,50 +249,50 @@ struct SkelWalk {
     if (ended) return;
     uint64_t ins = 0xFEDCBA9876543210ull;    // insignificant coefficients, nibble i = i-th
     int cnt = 16, off = 0;
-    int tt = t, nn = n, BB = B;
+    int P = 26 - t;                          // current plane
+    const int Pmin = 27 - pl;                // planes P >= Pmin exist (t < pl)
+    int nn = n, BB = B;
     uint32_t sg = sig, ng = negm, sl = sig_last;
+    int aa = 0;      // the last hit emptied the remainder: plane P ends without a flag
     while (true) {
       const uint32_t x = bw.w0;
-      const int m = (int)clz32(x);
-      const uint32_t y = fsl(x, 0u, (uint32_t)(m + 1 > 32 ? 32 : m + 1));
-      const int z = (int)clz32(y);
+      const uint32_t m0 = clz_sh(x);         // zero flags (0xFFFFFFFF if x == 0)
+      const uint32_t y = fsl(x, 0u, m0 + 1u);
+      const uint32_t z = clz_sh(y);          // run before the hit (0xFFFFFFFF: none in w0)
+      const int m = (int)m0 + aa;            // planes ended by this token
       const int base = m ? 0 : off;
-      const int k = m + z + 3;
-      const int cost = m * (nn + 1) + z + 3;
-      if (z >= cnt - base || k > 32 || tt + m >= pl || cost > BB) break;
+      const int cost = (int)m0 * (nn + 1) + aa * nn + (int)z + 3;
+      // fast iff: a hit among the remainder, the token inside w0 (m0 + z + 3
+      // <= 32), every crossed plane exists and the budget covers the token
+      const int chk = (29 - (int)m0 - (int)z) | (P - m - Pmin) | (BB - cost);
+      if (!(z < (uint32_t)(cnt - base) && chk >= 0)) break;
 #if !defined(__CUDA_ARCH__)
       ++fast_iters;
 #endif
-      const uint32_t sgn = (y >> (30 - z)) & 1u;
-      adv<REFILL>(bw, (uint32_t)k);
+      const uint32_t sgn = (y >> (30u - z)) & 1u;
+      adv<REFILL>(bw, m0 + z + 3u);
       BB -= cost;
-      tt += m;
-      if (m) sl = sg;
-      const int a = base + z;
+      P -= m;
+      if (m) sl = sg;                        // sig at the refinement of plane P
+      const int a = base + (int)z;
       const uint32_t c = (uint32_t)(ins >> (4 * a)) & 15u;
       const uint64_t lowm = (1ull << (4 * a)) - 1ull;
       ins = (ins & lowm) | ((ins >> 4) & ~lowm);
       cnt -= 1;
-      psig[c] = (uint8_t)(26 - tt);
-      const uint32_t h = 1u << c;
-      sg |= h;
+      psig[c] = (uint8_t)P;
+      sg |= 1u << c;
       ng |= sgn << c;
       nn += 1;
       off = a;
-      if (a == cnt) {                        // remainder empty: the plane ends without a flag
-        if (cnt == 0 || tt + 1 >= pl || nn > BB) break;
-        tt += 1;
-        BB -= nn;
-        sl = sg;
-        off = 0;
-      }
+      aa = a == cnt;
     }
-    t = tt; n = nn; B = BB; sig = sg; negm = ng;
+    t = 26 - P; n = nn; B = BB; sig = sg; negm = ng;
     sig_last = sl;
-    p_last = 26 - tt;
+    p_last = P;
     cut = (int)popc32(sl);
     // eligible remainder of plane t = ins[off:], i.e. every coefficient from
-    // ins[off] up (all lower ones are significant or already skipped)
+    // ins[off] up (all lower ones are significant or already skipped); empty
+    // when the last hit took the remainder's last member (run_from ends the plane)
     rem_lo = off == 0 ? 0xFFFFu
            : off >= cnt ? 0u : (0xFFFFu << (uint32_t)((ins >> (4 * off)) & 15u)) & 0xFFFFu;
   }
