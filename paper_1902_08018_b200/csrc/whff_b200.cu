@@ -329,6 +329,22 @@ __device__ __forceinline__ void acc_coeff(Acc& A, int policy, const Decoded& d, 
   }
 }
 
+// Coefficient-domain accumulator fed by the fields loop of decode_block_sf:
+// w[r] += q_c * u[j] for each significant coefficient c at raster (r, j),
+// in coefficient order (identical arithmetic to acc_coeff, which also adds
+// the zero coefficients as exact no-ops).
+struct CoefSink {
+  float u[4];
+  float w[4];
+  template <int C>
+  __device__ __forceinline__ void coef(uint32_t mag, uint32_t negm) {
+    constexpr int pos = seq_pos(C);
+    float q = __uint2float_rn(mag);
+    q = __uint_as_float(__float_as_uint(q) ^ ((negm << (31 - C)) & 0x80000000u));
+    w[pos >> 2] = __fmaf_rn(q, u[pos & 3], w[pos >> 2]);
+  }
+};
+
 template <int VAR>
 struct VarTraits;
 // 0: FixedRate(8) implicit index, one 16-byte load per block, no refill
@@ -403,12 +419,22 @@ __global__ void WHFF_GEMV_LB k_decode_gemv(JobTable T, int policy,
     const uint64_t b = row_block0 + bcol;
     BitWin bw;
     Decoded d;
+    // coefficient domain + skeleton-first: accumulate inside the fields loop
+    constexpr bool kSink = SF && EVAL == WHFF_EVAL_COEFF;
+    CoefSink cs;
+    if (kSink) {
+      const float4 u4 = active ? ldg(U + bcol) : make_float4(0.f, 0.f, 0.f, 0.f);
+      cs.u[0] = u4.x; cs.u[1] = u4.y; cs.u[2] = u4.z; cs.u[3] = u4.w;
+#pragma unroll
+      for (int a = 0; a < 4; ++a) cs.w[a] = 0.0f;
+    }
     if (VAR == 0) {
       const uint4 q = nxt;
       const uint64_t bn = bcol + 32 * kGemvWarps;
       if (bn < bc) nxt = ldg(seg128 + row_block0 + bn);   // prefetch this warp's next group
       win_128(bw, q.x, q.y, q.z, q.w, active ? clamp_len(b * 128ull, 128ull, s.payload_bits) : 0);
-      if (SF) decode_block_sf<false, false>(bw, pl, d);
+      if (kSink) decode_block_sf<false, false>(bw, pl, d, cs);
+      else if (SF) decode_block_sf<false, false>(bw, pl, d);
       else decode_block<false, false, false>(bw, pl, d, 0xFFFFFFFFu);
     } else {
       uint64_t start = 0;
@@ -440,10 +466,12 @@ __global__ void WHFF_GEMV_LB k_decode_gemv(JobTable T, int policy,
         bw.src = s.words;
       }
       if (__any_sync(0xFFFFFFFFu, active && !fits_no_refill(start, len))) {
-        if (SF) decode_block_sf<TR::kRaw, true>(bw, pl, d);
+        if (kSink) decode_block_sf<TR::kRaw, true>(bw, pl, d, cs);
+        else if (SF) decode_block_sf<TR::kRaw, true>(bw, pl, d);
         else decode_block<TR::kRaw, true>(bw, pl, d, 0xFFFFFFFFu);
       } else {
-        if (SF) decode_block_sf<TR::kRaw, false>(bw, pl, d);
+        if (kSink) decode_block_sf<TR::kRaw, false>(bw, pl, d, cs);
+        else if (SF) decode_block_sf<TR::kRaw, false>(bw, pl, d);
         else decode_block<TR::kRaw, false>(bw, pl, d, 0xFFFFFFFFu);
       }
     }
@@ -458,7 +486,17 @@ __global__ void WHFF_GEMV_LB k_decode_gemv(JobTable T, int policy,
     } else {
       const int k = (int)d.emax - kEmaxBias - kQuantBits;
       if (!d.raw && d.emax != 0 && k >= -126 && k <= 100) {
-        acc_coeff(A, policy, d, ldg(U + bcol), k);
+        if (kSink) {
+          const float sc = scale_f32(k);
+#pragma unroll
+          for (int a = 0; a < 4; ++a) {
+            const float t = __fmul_rn(cs.w[a], sc);
+            if (policy == WHFF_POLICY_SINGLE) A.f[a] = __fadd_rn(A.f[a], t);
+            else A.d[a] = __dadd_rn(A.d[a], (double)t);
+          }
+        } else {
+          acc_coeff(A, policy, d, ldg(U + bcol), k);
+        }
       } else if (d.raw || d.emax != 0) {   // raw escape / extreme scale: exact spatial path
         const float4 v4 = load_v4(v, bcol, s.cols, v_aligned);
         float x[16];

@@ -27,6 +27,7 @@
 // consecutive blocks) stay converged.
 #pragma once
 #include <stdint.h>
+#include <type_traits>
 
 #if defined(__CUDACC__)
 #define WHFF_HD __host__ __device__ __forceinline__
@@ -143,6 +144,22 @@ WHFF_HD uint32_t fsl(uint32_t hi, uint32_t lo, uint32_t s) {  // s in [0, 32]
 #else
   return s >= 32 ? lo : (s ? (hi << s) | (lo >> (32 - s)) : hi);
 #endif
+}
+// low 32 bits of (hi:lo) >> s, s in [0, 32] (clamped)
+WHFF_HD uint32_t fsr(uint32_t lo, uint32_t hi, uint32_t s) {
+#if defined(__CUDA_ARCH__)
+  return __funnelshift_rc(lo, hi, s);
+#else
+  return s >= 32 ? hi : (s ? (lo >> s) | (hi << (32 - s)) : lo);
+#endif
+}
+// f(std::integral_constant<int, 0..15>) in order, fully unrolled
+template <int I = 0, class F>
+WHFF_HD void unroll16(F&& f) {
+  if constexpr (I < 16) {
+    f(std::integral_constant<int, I>());
+    unroll16<I + 1>(f);
+  }
 }
 WHFF_HD uint32_t top_mask(int nbits) {  // top nbits set, nbits in [0, 32]
   return nbits <= 0 ? 0u : (nbits >= 32 ? 0xFFFFFFFFu : ~(0xFFFFFFFFu >> nbits));

@@ -408,8 +408,15 @@ struct SkelWalk {
   }
 };
 
-template <bool HAS_RAW, bool REFILL>
-WHFF_HD void decode_block_sf(BitWin& bw, int planes_limit, Decoded& d) {
+// Per-coefficient consumer of the fields loop (the fused GEMV's coefficient-
+// domain accumulator plugs in here); the default does nothing.
+struct NullSink {
+  template <int C>
+  WHFF_HD void coef(uint32_t, uint32_t) {}
+};
+
+template <bool HAS_RAW, bool REFILL, class Sink = NullSink>
+WHFF_HD void decode_block_sf(BitWin& bw, int planes_limit, Decoded& d, Sink&& sink = Sink()) {
   const int len = bw.len;
   d.negm = 0;
   d.emax = 0;
@@ -469,8 +476,9 @@ WHFF_HD void decode_block_sf(BitWin& bw, int planes_limit, Decoded& d) {
 #else
   for (int i = 0; i < 4; ++i) pv[i] = psw[i];
 #endif
-#pragma unroll
-  for (int c = 0; c < 16; ++c) {
+  const uint32_t negm = w.negm;
+  unroll16([&](auto cc) {
+    constexpr int c = decltype(cc)::value;
     if ((sig >> c) & 1u) {                   // skipped when no lane of the warp has it
       const uint32_t ps = (pv[c >> 2] >> (8 * (c & 3))) & 0xFFu;
       uint32_t e = ps;
@@ -479,10 +487,12 @@ WHFF_HD void decode_block_sf(BitWin& bw, int planes_limit, Decoded& d) {
         ++rank;
       }
       const uint32_t F = bw.w0;
-      d.mag[c] = (((F >> 1) | 0x80000000u) >> (31u - ps)) & (0xFFFFFFFFu << e);
+      const uint32_t mag = fsr(F, 1u, 32u - ps) & (0xFFFFFFFFu << e);
+      d.mag[c] = mag;
+      sink.template coef<c>(mag, negm);
       adv<REFILL>(bw, ps - e);
     }
-  }
+  });
   d.consumed = bw.pos;
 }
 
