@@ -68,6 +68,15 @@ WHFF_HD uint32_t clz_sh(uint32_t x) {
   return x ? (uint32_t)__builtin_clz(x) : 0xFFFFFFFFu;
 #endif
 }
+// OR over the lanes currently converged with this one (a superset of the
+// lane's own bits, whatever the grouping); the value itself on the host
+WHFF_HD uint32_t warp_or(uint32_t x) {
+#if defined(__CUDA_ARCH__)
+  return __reduce_or_sync(__activemask(), x);
+#else
+  return x;
+#endif
+}
 WHFF_HD uint32_t popc32(uint32_t x) {
 #if defined(__CUDA_ARCH__)
   return (uint32_t)__popc(x);
