@@ -333,6 +333,13 @@ __device__ __forceinline__ void acc_coeff(Acc& A, int policy, const Decoded& d, 
 // w[r] += q_c * u[j] for each significant coefficient c at raster (r, j),
 // in coefficient order (identical arithmetic to acc_coeff, which also adds
 // the zero coefficients as exact no-ops).
+// blocks the coefficient domain evaluates (zero blocks trivially): not a raw
+// escape, and a scale 2^k with k in [-126, 100] (no fp32 over/underflow)
+__device__ __forceinline__ bool coef_ok(const Decoded& d) {
+  const int k = (int)d.emax - kEmaxBias - kQuantBits;
+  return !d.raw && (d.emax == 0 || (k >= -126 && k <= 100));
+}
+
 struct CoefSink {
   float u[4];
   float w[4];
@@ -344,6 +351,25 @@ struct CoefSink {
     w[pos >> 2] = __fmaf_rn(q, u[pos & 3], w[pos >> 2]);
   }
 };
+
+// Coefficient-domain kernels: the rare blocks coef_ok() rejects (raw
+// escapes, extreme scales) are re-decoded here with their exact words and
+// accumulated in the spatial domain.  Out of line so the hot loop keeps its
+// register budget (64) and its instruction footprint.
+template <bool HAS_RAW>
+__device__ __noinline__ void coef_fallback(const uint32_t* words, uint64_t start, int len, int pl,
+                                           const float* v, uint64_t bcol, uint64_t cols,
+                                           bool v_aligned, uint32_t colmask, int policy, Acc* R) {
+  BitWin bw;
+  win_at(bw, words, start, len);
+  Decoded d;
+  decode_block_sf<HAS_RAW, true>(bw, pl, d);
+  if (!d.raw && d.emax == 0) return;
+  const float4 v4 = load_v4(v, bcol, cols, v_aligned);
+  float x[16];
+  reconstruct_words(d, x);
+  acc_exact(*R, policy, x, v4, colmask);
+}
 
 template <int VAR>
 struct VarTraits;
@@ -419,6 +445,8 @@ __global__ void WHFF_GEMV_LB k_decode_gemv(JobTable T, int policy,
     const uint64_t b = row_block0 + bcol;
     BitWin bw;
     Decoded d;
+    uint64_t fb_start = b * 128ull;          // the block's segment (coefficient fallback)
+    int fb_len = 0;
     // coefficient domain + skeleton-first: accumulate inside the fields loop
     constexpr bool kSink = SF && EVAL == WHFF_EVAL_COEFF;
     CoefSink cs;
@@ -432,8 +460,9 @@ __global__ void WHFF_GEMV_LB k_decode_gemv(JobTable T, int policy,
       const uint4 q = nxt;
       const uint64_t bn = bcol + 32 * kGemvWarps;
       if (bn < bc) nxt = ldg(seg128 + row_block0 + bn);   // prefetch this warp's next group
-      win_128(bw, q.x, q.y, q.z, q.w, active ? clamp_len(b * 128ull, 128ull, s.payload_bits) : 0);
-      if (kSink) decode_block_sf<false, false>(bw, pl, d, cs);
+      fb_len = active ? clamp_len(b * 128ull, 128ull, s.payload_bits) : 0;
+      win_128(bw, q.x, q.y, q.z, q.w, fb_len);
+      if (kSink) decode_block_sf<false, false, CoefSink&, false>(bw, pl, d, cs);
       else if (SF) decode_block_sf<false, false>(bw, pl, d);
       else decode_block<false, false, false>(bw, pl, d, 0xFFFFFFFFu);
     } else {
@@ -465,12 +494,14 @@ __global__ void WHFF_GEMV_LB k_decode_gemv(JobTable T, int policy,
         bw.avail = 128;
         bw.src = s.words;
       }
+      fb_start = start;
+      fb_len = len;
       if (__any_sync(0xFFFFFFFFu, active && !fits_no_refill(start, len))) {
-        if (kSink) decode_block_sf<TR::kRaw, true>(bw, pl, d, cs);
+        if (kSink) decode_block_sf<TR::kRaw, true, CoefSink&, false>(bw, pl, d, cs);
         else if (SF) decode_block_sf<TR::kRaw, true>(bw, pl, d);
         else decode_block<TR::kRaw, true>(bw, pl, d, 0xFFFFFFFFu);
       } else {
-        if (kSink) decode_block_sf<TR::kRaw, false>(bw, pl, d, cs);
+        if (kSink) decode_block_sf<TR::kRaw, false, CoefSink&, false>(bw, pl, d, cs);
         else if (SF) decode_block_sf<TR::kRaw, false>(bw, pl, d);
         else decode_block<TR::kRaw, false>(bw, pl, d, 0xFFFFFFFFu);
       }
@@ -485,7 +516,17 @@ __global__ void WHFF_GEMV_LB k_decode_gemv(JobTable T, int policy,
       acc_exact(A, policy, x, v4, colmask);
     } else {
       const int k = (int)d.emax - kEmaxBias - kQuantBits;
-      if (!d.raw && d.emax != 0 && k >= -126 && k <= 100) {
+      if (kSink && !coef_ok(d)) {
+        Acc R;
+#pragma unroll
+        for (int i = 0; i < 4; ++i) { R.d[i] = accR[i]; R.f[i] = accRf[i]; }
+        R.probe = A.probe;
+        coef_fallback<TR::kRaw>(s.words, fb_start, fb_len, pl, v, bcol, s.cols, v_aligned, colmask,
+                                policy, &R);
+#pragma unroll
+        for (int i = 0; i < 4; ++i) { accR[i] = R.d[i]; accRf[i] = R.f[i]; }
+        A.probe = R.probe;
+      } else if (coef_ok(d) && d.emax != 0) {
         if (kSink) {
           const float sc = scale_f32(k);
 #pragma unroll

@@ -415,14 +415,18 @@ struct NullSink {
   WHFF_HD void coef(uint32_t, uint32_t) {}
 };
 
-template <bool HAS_RAW, bool REFILL, class Sink = NullSink>
+// MAGS = false: only the sink sees the magnitudes (d.mag is left unset, and
+// so are raw-escape words: the caller re-decodes such blocks with MAGS).
+template <bool HAS_RAW, bool REFILL, class Sink = NullSink, bool MAGS = true>
 WHFF_HD void decode_block_sf(BitWin& bw, int planes_limit, Decoded& d, Sink&& sink = Sink()) {
   const int len = bw.len;
   d.negm = 0;
   d.emax = 0;
   d.raw = 0;
+  if (MAGS) {
 #pragma unroll
-  for (int c = 0; c < 16; ++c) d.mag[c] = 0;
+    for (int c = 0; c < 16; ++c) d.mag[c] = 0;
+  }
   if (len < 9) { d.consumed = len < 0 ? 0 : len; return; }
   const uint32_t hdr = bw.w0;
   const uint32_t code = hdr >> 23;
@@ -433,6 +437,7 @@ WHFF_HD void decode_block_sf(BitWin& bw, int planes_limit, Decoded& d, Sink&& si
     if ((hdr >> 22) & 1u) {                  // raw escape: same as WHFZ
       adv<REFILL>(bw, 10);
       d.raw = 1;
+      if (!MAGS) return;
       int nw = (len - 10) >> 5;
       if (nw > 16) nw = 16;
 #pragma unroll
@@ -488,7 +493,7 @@ WHFF_HD void decode_block_sf(BitWin& bw, int planes_limit, Decoded& d, Sink&& si
       }
       const uint32_t F = bw.w0;
       const uint32_t mag = fsr(F, 1u, 32u - ps) & (0xFFFFFFFFu << e);
-      d.mag[c] = mag;
+      if (MAGS) d.mag[c] = mag;
       sink.template coef<c>(mag, negm);
       adv<REFILL>(bw, ps - e);
     }

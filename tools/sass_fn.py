@@ -14,7 +14,7 @@ for ln in out.splitlines():
     if m:
         cur = m.group(1)
         continue
-    if cur == want and re.match(r"\s+/\*[0-9a-f]{4}\*/", ln):
+    if cur == want and re.match(r"\s+/\*[0-9a-f]{4,}\*/", ln):
         lines.append(ln)
 if "--mix" in sys.argv:
     mix = collections.Counter()
