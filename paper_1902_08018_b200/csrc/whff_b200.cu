@@ -371,6 +371,73 @@ __device__ __noinline__ void coef_fallback(const uint32_t* words, uint64_t start
   acc_exact(*R, policy, x, v4, colmask);
 }
 
+constexpr int kGemvWarps = 8;
+
+// Software-pipelined segment location for indexed / implicit variable-rate
+// streams (see k_decode_gemv).  Holds, for the next group, its start bit,
+// length and first four payload words, and for the group after it the
+// lane's raw index entries.
+template <bool INDEXED>
+struct SegPrefetch {
+  uint64_t start = 0;
+  int len = 0;
+  uint32_t a0 = 0, a1 = 0, a2 = 0, a3 = 0;
+  uint32_t il = 0;      // index entries of group gi (lens / starts, base)
+  uint64_t ib = 0;
+
+  __device__ __forceinline__ void load_index(const StreamView& s, uint64_t brow, uint64_t row_block0,
+                                             uint64_t bc, uint64_t gi, int lane) {
+    if (!INDEXED || gi >= s.gpr) return;
+    const uint64_t bcol = gi * 32 + lane;
+    const bool act = bcol < bc;
+    const uint64_t b = row_block0 + bcol;
+    il = act ? (uint32_t)s.lens[b] : 0u;
+    if (s.kind == WHFF_INDEX_COMPACT) ib = s.base[brow * s.gpr + gi];
+    else ib = act ? s.starts[b] : 0ull;
+  }
+  // locate group gn (its index entries are in il/ib) and load its words
+  __device__ __forceinline__ void locate(const StreamView& s, uint64_t row_block0, uint64_t bc,
+                                         uint64_t gn, int lane) {
+    if (gn >= s.gpr) return;                 // warp-uniform
+    const uint64_t bcol = gn * 32 + lane;
+    const bool act = bcol < bc;
+    const uint64_t b = row_block0 + bcol;
+    len = 0;
+    if (!INDEXED) {
+      start = b * (uint64_t)s.seg_bits;
+      if (act) len = clamp_len(start, s.seg_bits, s.payload_bits);
+    } else if (s.kind == WHFF_INDEX_COMPACT) {
+      uint32_t incl = il;
+#pragma unroll
+      for (int o = 1; o < 32; o <<= 1) {
+        const uint32_t t = __shfl_up_sync(0xFFFFFFFFu, incl, o);
+        if (lane >= o) incl += t;
+      }
+      start = ib + (incl - il);
+      if (act) len = clamp_len(start, il, s.payload_bits);
+    } else {
+      start = ib;
+      if (act) len = clamp_len(start, il, s.payload_bits);
+    }
+    if (act) {
+      const uint32_t* p = s.words + (start >> 5);
+      a0 = ldg(p); a1 = ldg(p + 1); a2 = ldg(p + 2); a3 = ldg(p + 3);
+    }
+  }
+  __device__ __forceinline__ void prologue(const StreamView& s, uint64_t brow, uint64_t row_block0,
+                                           uint64_t bc, uint64_t g0, int lane) {
+    load_index(s, brow, row_block0, bc, g0, lane);
+    locate(s, row_block0, bc, g0, lane);
+    load_index(s, brow, row_block0, bc, g0 + kGemvWarps, lane);
+  }
+  // called at group g with gn = g + 8: locate gn, fetch the index of gn + 8
+  __device__ __forceinline__ void advance(const StreamView& s, uint64_t brow, uint64_t row_block0,
+                                          uint64_t bc, uint64_t gn, int lane) {
+    locate(s, row_block0, bc, gn, lane);
+    load_index(s, brow, row_block0, bc, gn + kGemvWarps, lane);
+  }
+};
+
 template <int VAR>
 struct VarTraits;
 // 0: FixedRate(8) implicit index, one 16-byte load per block, no refill
@@ -382,7 +449,6 @@ template <> struct VarTraits<2> { static constexpr bool kRefill = true, kRaw = f
 // 3: indexed with raw flag (fixed accuracy)
 template <> struct VarTraits<3> { static constexpr bool kRefill = true, kRaw = true, kIndexed = true; };
 
-constexpr int kGemvWarps = 8;
 // launch bounds: plain 256 lets ptxas settle at 64 registers (4 CTAs/SM),
 // measured best for the fused kernel; -DWHFF_GEMV_MINB=n overrides for sweeps
 #ifdef WHFF_GEMV_MINB
@@ -438,6 +504,11 @@ __global__ void WHFF_GEMV_LB k_decode_gemv(JobTable T, int policy,
     const uint64_t bcol0 = (uint64_t)warp * 32 + lane;
     if (bcol0 < bc) nxt = ldg(seg128 + row_block0 + bcol0);
   }
+  // Variable-length streams: the segment of group g+8 is located (index
+  // loaded one iteration earlier) and its four payload words are loaded
+  // while group g decodes; the index of g+16 is loaded at the same time.
+  SegPrefetch<TR::kIndexed> pf;
+  if (VAR != 0) pf.prologue(s, brow, row_block0, bc, (uint64_t)warp, lane);
 
   for (uint64_t g = warp; g < s.gpr; g += kGemvWarps) {
     const uint64_t bcol = g * 32 + lane;
@@ -466,27 +537,12 @@ __global__ void WHFF_GEMV_LB k_decode_gemv(JobTable T, int policy,
       else if (SF) decode_block_sf<false, false>(bw, pl, d);
       else decode_block<false, false, false>(bw, pl, d, 0xFFFFFFFFu);
     } else {
-      uint64_t start = 0;
-      int len = 0;
-      if (!TR::kIndexed) {
-        start = b * (uint64_t)s.seg_bits;
-        if (active) len = clamp_len(start, s.seg_bits, s.payload_bits);
-      } else if (s.kind == WHFF_INDEX_COMPACT) {
-        const uint32_t l = active ? (uint32_t)s.lens[b] : 0u;
-        uint32_t incl = l;
-#pragma unroll
-        for (int o = 1; o < 32; o <<= 1) {
-          const uint32_t t = __shfl_up_sync(0xFFFFFFFFu, incl, o);
-          if (lane >= o) incl += t;
-        }
-        start = s.base[brow * s.gpr + g] + (incl - l);
-        if (active) len = clamp_len(start, l, s.payload_bits);
-      } else if (active) {
-        start = s.starts[b];
-        len = clamp_len(start, s.lens[b], s.payload_bits);
-      }
+      const uint64_t start = pf.start;
+      const int len = pf.len;
+      const uint32_t a0 = pf.a0, a1 = pf.a1, a2 = pf.a2, a3 = pf.a3;
+      pf.advance(s, brow, row_block0, bc, g + kGemvWarps, lane);
       if (active) {
-        win_at(bw, s.words, start, len);
+        win_words(bw, s.words, start, len, a0, a1, a2, a3);
       } else {
         bw.w0 = bw.w1 = bw.w2 = bw.w3 = 0u;
         bw.pos = 0;

@@ -77,6 +77,21 @@ WHFF_HD uint32_t warp_or(uint32_t x) {
   return x;
 #endif
 }
+// floor(a / d) for 0 <= a < 2^16, 1 <= d <= 16 without the integer-division
+// sequence: a * rcp.approx(d) is within 0.02 of a / d, so its truncation is
+// the quotient or one less (never more: a non-integer a/d sits >= 1/16 below
+// the next integer); one compare fixes it.
+WHFF_HD int small_div(int a, int d) {
+#if defined(__CUDA_ARCH__)
+  float r;
+  asm("rcp.approx.ftz.f32 %0, %1;" : "=f"(r) : "f"((float)d));
+  int q = __float2int_rz(__fmul_rn((float)a, r));
+  if ((q + 1) * d <= a) ++q;
+  return q;
+#else
+  return a / d;
+#endif
+}
 WHFF_HD uint32_t popc32(uint32_t x) {
 #if defined(__CUDA_ARCH__)
   return (uint32_t)__popc(x);
@@ -199,6 +214,27 @@ WHFF_HD void win_at(BitWin& b, const uint32_t* words, uint64_t bit, int len) {
   b.len = len;
   b.avail = 128 - (int)off;
   b.src = p + 4;
+  if (len < 128) {
+    b.w0 &= top_mask(len);
+    b.w1 &= top_mask(len - 32);
+    b.w2 &= top_mask(len - 64);
+    b.w3 &= top_mask(len - 96);
+  }
+}
+
+// win_at from the four LE payload words already loaded at words + (bit >> 5)
+WHFF_HD void win_words(BitWin& b, const uint32_t* words, uint64_t bit, int len, uint32_t x0,
+                       uint32_t x1, uint32_t x2, uint32_t x3) {
+  const uint32_t off = (uint32_t)(bit & 31);
+  const uint32_t a0 = bswap32(x0), a1 = bswap32(x1), a2 = bswap32(x2), a3 = bswap32(x3);
+  b.w0 = fsl(a0, a1, off);
+  b.w1 = fsl(a1, a2, off);
+  b.w2 = fsl(a2, a3, off);
+  b.w3 = fsl(a3, 0u, off);
+  b.pos = 0;
+  b.len = len;
+  b.avail = 128 - (int)off;
+  b.src = words + (bit >> 5) + 4;
   if (len < 128) {
     b.w0 &= top_mask(len);
     b.w1 &= top_mask(len - 32);

@@ -326,7 +326,7 @@ struct SkelWalk {
         int m = zf;
         const int planes_left = pl - 1 - t;
         if (m > planes_left) m = planes_left;
-        if (m * (n + 1) > B) m = B / (n + 1);    // budget boundary (once per block)
+        if (m * (n + 1) > B) m = small_div(B, n + 1);    // budget boundary (once per block)
         if (m > 0) {
           adv<REFILL>(bw, (uint32_t)m);
           B -= m * (n + 1);
