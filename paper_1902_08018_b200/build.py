@@ -46,7 +46,9 @@ def stale():
 def build(force=False, verbose=False):
     if not force and not stale():
         return LIB
-    cmd = [nvcc(), *NVCC_FLAGS, "-I", os.path.join(ROOT, "include"), "-o", LIB + ".tmp", *SOURCES]
+    extra = os.environ.get("WHFF_NVCC_EXTRA", "").split()   # tuning sweeps (-D...)
+    cmd = [nvcc(), *NVCC_FLAGS, *extra, "-I", os.path.join(ROOT, "include"), "-o", LIB + ".tmp",
+           *SOURCES]
     if verbose:
         print(" ".join(cmd), file=sys.stderr)
     env = dict(os.environ)
