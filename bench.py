@@ -40,7 +40,10 @@ def parse():
     ap.add_argument("--warmup", type=int, default=5)
     ap.add_argument("--impl", default="b200", choices=["b200", "reference"])
     ap.add_argument("--mode", default="rate:8", help="rate:BPV | precision:P | accuracy:TOL")
-    ap.add_argument("--evaluation", default="exact", choices=["exact", "coefficient"])
+    ap.add_argument("--evaluation", default="coefficient", choices=["exact", "coefficient"],
+                    help="coefficient: accumulate 2^k Q (G^T v) per block and apply the inverse "
+                         "lift G once per block-row (SURVEY 7, hard part 2); exact: decoded "
+                         "binary32 words x v, the reference's products")
     ap.add_argument("--layout", default="skeleton-first", choices=["reference", "skeleton-first"],
                     help="device payload layout (whff_dstream_relayout): a per-block bit "
                          "permutation of the WHFZ stream, same bytes, same decoded words")
@@ -471,9 +474,11 @@ def b200_main(args, world, rank, local):
     try:
         with open(os.path.join(ROOT, "profiles", "ncu_traffic.json")) as fh:
             tj = json.load(fh)
-            if (tj.get("mode") == args.mode and tj.get("evaluation") == args.evaluation
-                    and tj.get("layout", "reference") == args.layout):
-                traffic = tj.get("dram_bytes_per_launch")
+        for e in (tj if isinstance(tj, list) else [tj]):
+            if (e.get("mode") == args.mode and e.get("evaluation") == args.evaluation
+                    and e.get("layout", "reference") == args.layout
+                    and e.get("slits", 52) == args.slits):
+                traffic = e.get("dram_bytes_per_launch")
     except Exception:
         pass
     p50 = statistics.median(step_ms)

@@ -344,10 +344,10 @@ struct CoefSink {
   float u[4];
   float w[4];
   template <int C>
-  __device__ __forceinline__ void coef(uint32_t mag, uint32_t negm) {
+  __device__ __forceinline__ void coef(uint32_t mag, uint32_t sign31) {   // sign at bit 31
     constexpr int pos = seq_pos(C);
     float q = __uint2float_rn(mag);
-    q = __uint_as_float(__float_as_uint(q) ^ ((negm << (31 - C)) & 0x80000000u));
+    q = __uint_as_float(__float_as_uint(q) ^ (sign31 & 0x80000000u));
     w[pos >> 2] = __fmaf_rn(q, u[pos & 3], w[pos >> 2]);
   }
 };

@@ -199,7 +199,7 @@ template <bool REFILL>
 struct SkelWalk {
   BitWin& bw;
   uint8_t* psig;
-  uint32_t sig = 0, negm = 0;
+  uint32_t sig = 0;     // significant set; signs live in bit 7 of the psig bytes
   int n = 0;
   int B = 0;
   int t = 0;           // current plane index from the top (P = 26 - t)
@@ -252,7 +252,7 @@ struct SkelWalk {
     int P = 26 - t;                          // current plane
     const int Pmin = 27 - pl;                // planes P >= Pmin exist (t < pl)
     int nn = n, BB = B;
-    uint32_t sg = sig, ng = negm, sl = sig_last;
+    uint32_t sg = sig, sl = sig_last;
     int aa = 0;      // the last hit emptied the remainder: plane P ends without a flag
     while (true) {
       const uint32_t x = bw.w0;
@@ -269,7 +269,7 @@ struct SkelWalk {
 #if !defined(__CUDA_ARCH__)
       ++fast_iters;
 #endif
-      const uint32_t sgn = (y >> (30u - z)) & 1u;
+      const uint32_t sgn7 = (y >> (23u - z)) & 0x80u;   // the sign, at bit 7
       adv<REFILL>(bw, m0 + z + 3u);
       BB -= cost;
       P -= m;
@@ -279,14 +279,13 @@ struct SkelWalk {
       const uint64_t lowm = (1ull << (4 * a)) - 1ull;
       ins = (ins & lowm) | ((ins >> 4) & ~lowm);
       cnt -= 1;
-      psig[c] = (uint8_t)P;
+      psig[c] = (uint8_t)(P | sgn7);
       sg |= 1u << c;
-      ng |= sgn << c;
       nn += 1;
       off = a;
       aa = a == cnt;
     }
-    t = 26 - P; n = nn; B = BB; sig = sg; negm = ng;
+    t = 26 - P; n = nn; B = BB; sig = sg;
     sig_last = sl;
     p_last = P;
     cut = (int)popc32(sl);
@@ -388,9 +387,8 @@ struct SkelWalk {
       const uint32_t h = rem & (0u - rem);
       rem ^= h;
       krem -= z + 1;
-      psig[31 - clz32(h)] = (uint8_t)P;
+      psig[31 - clz32(h)] = (uint8_t)(P | (sgn << 7));
       sig |= h;
-      if (sgn) negm |= h;
       n += 1;
       rem_lo = 0xFFFFu & ~(h | (h - 1u));
       if (krem == 0 || B == 0) {             // no further flag (remainder empty / budget)
@@ -461,7 +459,6 @@ WHFF_HD void decode_block_sf(BitWin& bw, int planes_limit, Decoded& d, Sink&& si
   SkelWalk<REFILL> w(bw, reinterpret_cast<uint8_t*>(psw));
   w.B = len - hbits;
   w.run(pl);
-  d.negm = w.negm;
   // Coefficient-major refinement fields, index order (K:326-332 bits).
   // Coefficient c, significant at plane ps, holds the bits of planes
   // ps-1 .. e: e = p_last+1 for the members of sig_last (one lower for the
@@ -481,11 +478,11 @@ WHFF_HD void decode_block_sf(BitWin& bw, int planes_limit, Decoded& d, Sink&& si
 #else
   for (int i = 0; i < 4; ++i) pv[i] = psw[i];
 #endif
-  const uint32_t negm = w.negm;
   unroll16([&](auto cc) {
     constexpr int c = decltype(cc)::value;
     if ((sig >> c) & 1u) {                   // skipped when no lane of the warp has it
-      const uint32_t ps = (pv[c >> 2] >> (8 * (c & 3))) & 0xFFu;
+      const uint32_t pb = pv[c >> 2] >> (8 * (c & 3));
+      const uint32_t ps = pb & 0x1Fu;
       uint32_t e = ps;
       if ((sig_last >> c) & 1u) {
         e = pl1 - (rank < cut ? 1u : 0u);
@@ -494,10 +491,16 @@ WHFF_HD void decode_block_sf(BitWin& bw, int planes_limit, Decoded& d, Sink&& si
       const uint32_t F = bw.w0;
       const uint32_t mag = fsr(F, 1u, 32u - ps) & (0xFFFFFFFFu << e);
       if (MAGS) d.mag[c] = mag;
-      sink.template coef<c>(mag, negm);
+      sink.template coef<c>(mag, pb << 24);  // sign at bit 31
       adv<REFILL>(bw, ps - e);
     }
   });
+  if (MAGS) {                                // signs: bit 7 of each psig byte
+    uint32_t nm = 0;
+#pragma unroll
+    for (int i = 0; i < 4; ++i) nm |= (((pv[i] & 0x80808080u) * 0x00204081u) >> 28) << (4 * i);
+    d.negm = nm;
+  }
   d.consumed = bw.pos;
 }
 
@@ -536,7 +539,7 @@ WHFF_HD void unrelayout_segment(const uint32_t* in_words, uint32_t* out_words, u
   for (int c = 0; c < 16; ++c) {
     int l = 0;
     if ((w.sig >> c) & 1u) {
-      l = psig[c] - 1 - w.p_last;
+      l = (psig[c] & 0x1F) - 1 - w.p_last;   // bit 7 holds the sign
       l = l < 0 ? 0 : l;
       if ((w.sig_last >> c) & 1u) {
         const int rank = (int)popc32(w.sig_last & ((1u << c) - 1u));
