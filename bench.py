@@ -477,7 +477,7 @@ def b200_main(args, world, rank, local):
         for e in (tj if isinstance(tj, list) else [tj]):
             if (e.get("mode") == args.mode and e.get("evaluation") == args.evaluation
                     and e.get("layout", "reference") == args.layout
-                    and e.get("slits", 52) == args.slits):
+                    and e.get("slits", 52) == args.slits and e.get("S", 256000) == args.S):
                 traffic = e.get("dram_bytes_per_launch")
     except Exception:
         pass
