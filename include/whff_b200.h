@@ -258,6 +258,17 @@ whff_status_t whff_csr_matvec(const int64_t* indptr_dev, const int32_t* indices_
 whff_status_t whff_source_term(const float* footprint_dev, const float* dark_dev, float dose,
                                uint64_t n, float* u_dev, whff_stream_t stream);
 
+/* ------------------------------------------------------------------ */
+/* Device clock for the real-time scan (pipeline.py:164-289, 290-345)   */
+/* ------------------------------------------------------------------ */
+
+/* *t_dev = the device's %globaltimer (ns), written in stream order.       */
+whff_status_t whff_device_timestamp(uint64_t* t_dev, whff_stream_t stream);
+/* Holds the stream until %globaltimer >= *base_dev + offset_ns: paces the
+ * schedule's millisecond steps on the device (replaces the reference's
+ * simulated clock / wall-clock producer thread).                          */
+whff_status_t whff_wait_until(const uint64_t* base_dev, uint64_t offset_ns, whff_stream_t stream);
+
 #ifdef __cplusplus
 }
 #endif

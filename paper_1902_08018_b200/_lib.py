@@ -69,6 +69,8 @@ _SIG = {
     "whff_find_nonfinite": ([_P, _U64, _P, _P], _I),
     "whff_csr_matvec": ([_P, _P, _P, _U64, _P, _P, _P, _P, _P], _I),
     "whff_source_term": ([_P, _P, ctypes.c_float, _U64, _P, _P], _I),
+    "whff_device_timestamp": ([_P, _P], _I),
+    "whff_wait_until": ([_P, _U64, _P], _I),
 }
 
 _lib = None

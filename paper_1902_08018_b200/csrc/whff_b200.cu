@@ -852,6 +852,18 @@ __global__ void k_csr_matvec(const int64_t* indptr, const int32_t* indices, cons
   y[i] = __double2float_rn(acc);
 }
 
+// device clock for run_scan pacing (pipeline.py:164-289 real-time mode)
+__device__ __forceinline__ uint64_t globaltimer() {
+  uint64_t t;
+  asm volatile("mov.u64 %0, %%globaltimer;" : "=l"(t));
+  return t;
+}
+__global__ void k_timestamp(uint64_t* t) { *t = globaltimer(); }
+__global__ void k_wait_until(const uint64_t* base, uint64_t offset_ns) {
+  const uint64_t target = *base + offset_ns;
+  while (globaltimer() < target) __nanosleep(2000);
+}
+
 __global__ void k_source_term(const float* fp, const float* dark, float dose, uint64_t n, float* u) {
   const uint64_t i = blockIdx.x * (uint64_t)blockDim.x + threadIdx.x;
   if (i >= n) return;
@@ -1831,6 +1843,20 @@ whff_status_t whff_csr_matvec(const int64_t* indptr, const int32_t* indices, con
   if (n == 0) return WHFF_OK;
   k_csr_matvec<<<grid_for(n, 256), 256, 0, (cudaStream_t)stream>>>(indptr, indices, data, n, x, b, u, y);
   WCK_LAUNCH("csr_matvec");
+  return WHFF_OK;
+}
+
+whff_status_t whff_device_timestamp(uint64_t* t_dev, whff_stream_t stream) {
+  if (!t_dev) return fail(WHFF_ERR_ARGUMENT, "null argument");
+  k_timestamp<<<1, 1, 0, (cudaStream_t)stream>>>(t_dev);
+  WCK_LAUNCH("device_timestamp");
+  return WHFF_OK;
+}
+
+whff_status_t whff_wait_until(const uint64_t* base_dev, uint64_t offset_ns, whff_stream_t stream) {
+  if (!base_dev) return fail(WHFF_ERR_ARGUMENT, "null argument");
+  k_wait_until<<<1, 1, 0, (cudaStream_t)stream>>>(base_dev, offset_ns);
+  WCK_LAUNCH("wait_until");
   return WHFF_OK;
 }
 

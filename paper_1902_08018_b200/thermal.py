@@ -112,6 +112,53 @@ class ThermalState:
                    torch.zeros(S, dtype=torch.float32, device="cuda"))
 
 
+class HeatLoad:
+    """thermal.py:31-59: dark-phase load plus per-(field, slit) illumination
+    footprints (host arrays; DeviceHeatLoad holds the device copy)."""
+
+    def __init__(self, dark_load, light_footprints, dose_scale=1.0):
+        dark_load = np.asarray(dark_load, dtype=np.float32)
+        bad = np.flatnonzero(~np.isfinite(dark_load))
+        if bad.size:
+            raise NonFiniteError("dark_load", int(bad[0]))
+        self.dark_load = dark_load
+        self._footprints = {}
+        for key, fp in light_footprints.items():
+            fp = np.asarray(fp, dtype=np.float32)
+            bad = np.flatnonzero(~np.isfinite(fp))
+            if bad.size:
+                raise NonFiniteError(f"light_load{key}", int(bad[0]))
+            if (fp < 0).any():
+                raise WhffError(f"light footprint {key} has negative entries")
+            self._footprints[key] = fp
+        self.dose_scale = float(dose_scale)
+
+    def light_load(self, field_id, slit_id):
+        try:
+            return self._footprints[(field_id, slit_id)]
+        except KeyError:
+            raise WhffError(f"no light footprint for field {field_id} slit {slit_id}") from None
+
+    @property
+    def footprints(self):
+        return dict(self._footprints)
+
+
+def synthetic_heatload(model, seed=0, dose_scale=1.0, cooling=1e-3):
+    """thermal.py:62-78 (formulas and rng order in synth.heatload)."""
+    n_slits = {model.n_slits(f) for f in range(model.n_fields)}
+    if len(n_slits) != 1:
+        raise WhffError("synthetic_heatload expects the same slit count in every field")
+    dark, fps, dose = synth_heatload(model.spec, model.n_fields, n_slits.pop(), seed=seed,
+                                     dose_scale=dose_scale, cooling=cooling)
+    return HeatLoad(dark, fps, dose)
+
+
+def synth_heatload(*a, **k):
+    from .synth import heatload
+    return heatload(*a, **k)
+
+
 class DeviceHeatLoad:
     """Device copy of a reference HeatLoad (thermal.py:31-59)."""
 

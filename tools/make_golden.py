@@ -158,7 +158,38 @@ def pipeline_small():
     print("pipeline steps", len(slits))
 
 
+def scan_small():
+    """Reference run_scan (pipeline.py:164-181, simulated clock) on the
+    config-1 model: two fields of a shortened fast schedule, without
+    compression, with the default FixedAccuracy(1e-12) and with FixedRate(8).
+    Stores the deformations and the timing-independent trace columns."""
+    spec = model.ModelSpec(grid_rows=32, grid_cols=32, S=256, K=512, M=16, seed=7)
+    m = model.generate_model(spec)
+    sched = model.build_scan_schedule("fast", 2, t_l=6, t_d=3)
+    load = thermal.synthetic_heatload(m, seed=0)
+    out = {}
+    for tag, cfg in (("raw", pipeline.PipelineConfig()),
+                     ("acc", pipeline.PipelineConfig(use_compression=True)),
+                     ("r8", pipeline.PipelineConfig(use_compression=True,
+                                                    codec_mode=codec.FixedRate(8)))):
+        res = pipeline.run_scan(m, sched, load, cfg)
+        for a in model.AXES:
+            out[f"{tag}_D_{a}"] = res.deformations[a]
+        tr = res.trace.steps
+        out[f"{tag}_field"] = np.array([s.field_id for s in tr])
+        out[f"{tag}_k"] = np.array([s.k for s in tr])
+        out[f"{tag}_light"] = np.array([s.phase == "light" for s in tr])
+        out[f"{tag}_slit"] = np.array([s.slit for s in tr])
+        out[f"{tag}_bytes_in"] = np.array([s.bytes_in for s in tr])
+    np.savez_compressed(os.path.join(OUT, "scan_small.npz"), **out)
+    print("scan steps", len(tr))
+
+
 if __name__ == "__main__":
+    if len(sys.argv) > 1:
+        for name in sys.argv[1:]:
+            globals()[name]()
+        sys.exit(0)
     codec_cases()
     gemv_cases()
     thermal_cases()
