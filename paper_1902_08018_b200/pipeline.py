@@ -21,8 +21,9 @@ What changes:
     ``step_period_s`` set, each schedule step is held until its millisecond
     on the device clock (%globaltimer, whff_wait_until), so the trace is a
     real-time run; without it steps run back to back (throughput mode);
-  * a field's latency is the last delivery minus the field's start, judged
-    against its budget exactly as pipeline.py:287-289 / 339-344 do.
+  * a field's latency is its last delivery (end of its last light step)
+    minus the field's start, judged against its budget as the reference's
+    simulated clock does (pipeline.py:269-270, 285-289).
 
 Evaluations: "reference" decodes the slit words and runs the sequential mixed
 GEMV (bit-identical to the reference's decompress + gemv), "exact" and
@@ -282,7 +283,8 @@ def run_scan(model, schedule, heatload, cfg=None, resampler=None, backend=None):
             nbytes = slits[(fs.field_id, slit)].nbytes if phase == "light" else 0
             records.append(StepRecord(fs.field_id, k, phase, slit, nbytes, 0.0, 0.0,
                                       t_e[j] - t_s[j], t_s[j], t_s[j], t_s[j], t_e[j]))
-            last_delivery = max(last_delivery, t_e[j])
+            if phase == "light":             # a delivery (pipeline.py:269-270, 287)
+                last_delivery = t_e[j]
             j += 1
         latency = last_delivery - field_start
         budget = fs.time_budget_ms / 1e3
