@@ -463,8 +463,8 @@ WHFF_HD void decode_block_sf(BitWin& bw, int planes_limit, Decoded& d, Sink&& si
   // Coefficient c, significant at plane ps, holds the bits of planes
   // ps-1 .. e: e = p_last+1 for the members of sig_last (one lower for the
   // first `cut` of them, which got plane p_last's bit), e = ps otherwise.
-  // Its magnitude is the leading 1 at bit ps followed by the field:
-  // ((0x80000000 | F >> 1) >> (31 - ps)) with the bits below e cleared.
+  // Its magnitude is the leading 1 at bit ps followed by the l = ps - e field
+  // bits: funnelshift_r(F, 1, 32 - l) << e.
   const uint32_t sig = w.sig, sig_last = w.sig_last;
   const uint32_t pl1 = (uint32_t)(w.p_last + 1);
   const int cut = w.cut;
@@ -488,11 +488,11 @@ WHFF_HD void decode_block_sf(BitWin& bw, int planes_limit, Decoded& d, Sink&& si
         e = pl1 - (rank < cut ? 1u : 0u);
         ++rank;
       }
-      const uint32_t F = bw.w0;
-      const uint32_t mag = fsr(F, 1u, 32u - ps) & (0xFFFFFFFFu << e);
+      const uint32_t l = ps - e;             // field length
+      const uint32_t mag = fsr(bw.w0, 1u, 32u - l) << e;   // (1 : top l bits of F) << e
       if (MAGS) d.mag[c] = mag;
       sink.template coef<c>(mag, pb << 24);  // sign at bit 31
-      adv<REFILL>(bw, ps - e);
+      adv<REFILL>(bw, l);
     }
   });
   if (MAGS) {                                // signs: bit 7 of each psig byte
