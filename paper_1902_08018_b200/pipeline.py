@@ -140,7 +140,11 @@ class _Slit:
         self.streams, self.mats = [], []
         self.nbytes = 0
         for axis in AXES:
-            rows = model.slit_rows(axis, f, s, device=dev)
+            if hasattr(model, "slit_rows"):
+                rows = model.slit_rows(axis, f, s, device=dev)
+            else:                            # the reference's WaferModel (model.py:94-112)
+                rows = model.fetch_slit_submatrix(model.fetch_field_submatrix(axis, f), f, s)
+                rows = torch.from_numpy(np.ascontiguousarray(rows, np.float32)).to(dev)
             if cfg.use_compression:
                 ds = codec_mod.compress_device(rows, cfg.codec_mode)
                 self.nbytes += ds.payload_bytes
