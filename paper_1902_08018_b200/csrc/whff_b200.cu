@@ -457,10 +457,10 @@ template <> struct VarTraits<3> { static constexpr bool kRefill = true, kRaw = t
 #define WHFF_GEMV_LB __launch_bounds__(256)
 #endif
 
-template <int VAR, int EVAL, bool SF>
-__global__ void WHFF_GEMV_LB k_decode_gemv(JobTable T, int policy,
-                                                     unsigned long long* status) {
+template <int VAR, int EVAL, bool SF, int POL>
+__global__ void WHFF_GEMV_LB k_decode_gemv(JobTable T, unsigned long long* status) {
   using TR = VarTraits<VAR>;
+  constexpr int policy = POL;   // compile-time: only the policy's accumulators exist
   // one CTA per (job, block-row); its 8 warps split the row's 32-block groups
   const uint64_t gr = blockIdx.x;
   if (gr >= T.total_warps) return;
@@ -494,8 +494,12 @@ __global__ void WHFF_GEMV_LB k_decode_gemv(JobTable T, int policy,
 #pragma unroll
   for (int i = 0; i < 4; ++i) { A.d[i] = 0.0; A.f[i] = 0.0f; }
   A.probe = 0.0f;
-  double accR[4] = {0.0, 0.0, 0.0, 0.0};   // coefficient domain: exact raw-block part
-  float accRf[4] = {0.0f, 0.0f, 0.0f, 0.0f};
+  // coefficient domain: spatial part of the rare raw / extreme-scale blocks
+  // (its address goes to the out-of-line fallback, so it lives in local memory)
+  Acc RS;
+#pragma unroll
+  for (int i = 0; i < 4; ++i) { RS.d[i] = 0.0; RS.f[i] = 0.0f; }
+  RS.probe = 0.0f;
 
   const uint64_t row_block0 = brow * bc;
   const uint4* __restrict__ seg128 = reinterpret_cast<const uint4*>(s.words);
@@ -573,15 +577,8 @@ __global__ void WHFF_GEMV_LB k_decode_gemv(JobTable T, int policy,
     } else {
       const int k = (int)d.emax - kEmaxBias - kQuantBits;
       if (kSink && !coef_ok(d)) {
-        Acc R;
-#pragma unroll
-        for (int i = 0; i < 4; ++i) { R.d[i] = accR[i]; R.f[i] = accRf[i]; }
-        R.probe = A.probe;
         coef_fallback<TR::kRaw>(s.words, fb_start, fb_len, pl, v, bcol, s.cols, v_aligned, colmask,
-                                policy, &R);
-#pragma unroll
-        for (int i = 0; i < 4; ++i) { accR[i] = R.d[i]; accRf[i] = R.f[i]; }
-        A.probe = R.probe;
+                                policy, &RS);
       } else if (coef_ok(d) && d.emax != 0) {
         if (kSink) {
           const float sc = scale_f32(k);
@@ -598,18 +595,16 @@ __global__ void WHFF_GEMV_LB k_decode_gemv(JobTable T, int policy,
         const float4 v4 = load_v4(v, bcol, s.cols, v_aligned);
         float x[16];
         reconstruct_words(d, x);
-        Acc R;
-#pragma unroll
-        for (int i = 0; i < 4; ++i) { R.d[i] = accR[i]; R.f[i] = accRf[i]; }
-        R.probe = A.probe;
-        acc_exact(R, policy, x, v4, colmask);
-#pragma unroll
-        for (int i = 0; i < 4; ++i) { accR[i] = R.d[i]; accRf[i] = R.f[i]; }
-        A.probe = R.probe;
+        acc_exact(RS, policy, x, v4, colmask);
       }
     }
   }
 
+  double accR[4];
+  float accRf[4];
+#pragma unroll
+  for (int i = 0; i < 4; ++i) { accR[i] = RS.d[i]; accRf[i] = RS.f[i]; }
+  if (EVAL == WHFF_EVAL_COEFF) A.probe = __fadd_rn(A.probe, RS.probe);
   // fixed xor butterfly over the warp, then the 8 warps in order (deterministic)
 #pragma unroll
   for (int o = 16; o > 0; o >>= 1) {
@@ -1513,18 +1508,28 @@ static int variant_of(const whff_dstream* s) {
   return s->has_raw ? 3 : 2;
 }
 
+template <int EVAL, bool SF, int POL>
+static void launch_gemv_pol(int var, const JobTable& T, unsigned long long* status,
+                            cudaStream_t cs) {
+  const unsigned threads = 32 * kGemvWarps;
+  const unsigned blocks = (unsigned)T.total_warps;   // one CTA per block-row
+  switch (var) {
+    case 0: k_decode_gemv<0, EVAL, SF, POL><<<blocks, threads, 0, cs>>>(T, status); break;
+    case 1: k_decode_gemv<1, EVAL, SF, POL><<<blocks, threads, 0, cs>>>(T, status); break;
+    case 2: k_decode_gemv<2, EVAL, SF, POL><<<blocks, threads, 0, cs>>>(T, status); break;
+    default: k_decode_gemv<3, EVAL, SF, POL><<<blocks, threads, 0, cs>>>(T, status); break;
+  }
+}
+
 template <int EVAL, bool SF>
 static whff_status_t launch_gemv_var(int var, const JobTable& T, int policy,
                                      unsigned long long* status, cudaStream_t cs) {
-  const unsigned threads = 32 * kGemvWarps;
-  const unsigned blocks = (unsigned)T.total_warps;   // one CTA per block-row
-  if (blocks == 0) return WHFF_OK;
-  switch (var) {
-    case 0: k_decode_gemv<0, EVAL, SF><<<blocks, threads, 0, cs>>>(T, policy, status); break;
-    case 1: k_decode_gemv<1, EVAL, SF><<<blocks, threads, 0, cs>>>(T, policy, status); break;
-    case 2: k_decode_gemv<2, EVAL, SF><<<blocks, threads, 0, cs>>>(T, policy, status); break;
-    default: k_decode_gemv<3, EVAL, SF><<<blocks, threads, 0, cs>>>(T, policy, status); break;
-  }
+  if (T.total_warps == 0) return WHFF_OK;
+  if (policy == WHFF_POLICY_SINGLE) launch_gemv_pol<EVAL, SF, WHFF_POLICY_SINGLE>(var, T, status, cs);
+  else if (EVAL == WHFF_EVAL_COEFF || policy == WHFF_POLICY_MIXED)   // coefficient: mixed/single only
+    launch_gemv_pol<EVAL, SF, WHFF_POLICY_MIXED>(var, T, status, cs);
+  else launch_gemv_pol<EVAL, SF, (EVAL == WHFF_EVAL_COEFF ? WHFF_POLICY_MIXED : WHFF_POLICY_DOUBLE)>(
+      var, T, status, cs);
   WCK_LAUNCH("decode_gemv");
   return WHFF_OK;
 }
