@@ -285,6 +285,80 @@ struct SkelWalk {
       off = a;
       aa = a == cnt;
     }
+    // Closed-form ending.  From the loop's exit state the reference reads on
+    // until the budget or the plane limit stops it; when no further hit can
+    // become significant the result is (p_last, cut, sig_last, flag bits
+    // read) in closed form:
+    //  * a pending implicit plane end (aa) charges the next plane's refinement;
+    //  * the budget runs out inside the next run of zero flags: q complete
+    //    (flag + n-bit refinement) pairs, then r < n+1 bits = a zero flag and
+    //    r-1 refinement bits (or the flag that ends the last plane);
+    //  * or inside the next event token 0^m0 1 0^z 1 s: its m0 quiet planes are
+    //    complete and the hit or its sign is out of budget, so nothing changes.
+    // Anything else (all significant, a flag without a hit, a token beyond the
+    // window, plane limit inside a token) is run_from's.
+    if (nn < 16) {
+      int Pc = P, Bc = BB;
+      uint32_t slc = sl;
+      int offc = off;
+      bool done = false;
+      int pl_ = P, ct = 0, f = 0;
+      uint32_t sl_ = sl;
+      if (aa) {                              // implicit end of plane P (no flag)
+        if (Pc - 1 < Pmin) { done = true; pl_ = Pc; sl_ = slc; ct = (int)popc32(slc); }
+        else if (Bc < nn) { done = true; pl_ = Pc - 1; sl_ = sg; ct = Bc; }
+        else { Pc -= 1; Bc -= nn; slc = sg; offc = 0; }
+      }
+      if (!done) {
+        const uint32_t x = bw.w0;
+        const uint32_t zf = clz_sh(x);
+        const int m0 = zf > 32u ? 32 : (int)zf;    // zero flags available
+        const int per = nn + 1;
+        const int Q = Pc - Pmin;             // planes left below Pc
+        const int q = small_div(Bc, per);
+        const int r = Bc - q * per;
+        int need;                            // zero flags the closed form reads
+        if (q <= Q) {                        // the budget ends first
+          f = q + (r > 0);
+          need = f;
+          if (f <= m0) {
+            done = true;
+            if (r > 0 && q == Q) {           // that flag ends the last plane
+              pl_ = Pc - q; sl_ = q ? sg : slc; ct = q ? nn : (int)popc32(slc);
+            } else if (f == 0) {
+              pl_ = Pc; sl_ = slc; ct = (int)popc32(slc);
+            } else {
+              pl_ = Pc - f; sl_ = sg; ct = r > 0 ? r - 1 : nn;
+            }
+          }
+        } else {                             // the planes end first (budget to spare)
+          need = Q + 1;
+          if (Q + 1 <= m0) {
+            done = true;
+            f = Q + 1;
+            pl_ = Pc - Q; sl_ = Q ? sg : slc; ct = Q ? nn : (int)popc32(slc);
+          }
+        }
+        if (!done && m0 < need && m0 <= Q) {   // an event token comes first
+          const uint32_t y = fsl(x, 0u, (uint32_t)m0 + 1u);
+          const int z = (int)clz32(y);
+          const int krem = cnt - (m0 ? 0 : offc);
+          const int b2 = Bc - m0 * per;
+          if (z < krem && b2 < z + 3 && m0 + z + 3 <= 32) {
+            done = true;
+            f = m0 + (b2 < z + 2 ? b2 : z + 2);
+            pl_ = Pc - m0; sl_ = m0 ? sg : slc; ct = m0 ? nn : (int)popc32(slc);
+          }
+        }
+      }
+      if (done) {
+        adv<REFILL>(bw, (uint32_t)f);
+        n = nn; sig = sg; B = 0;
+        sig_last = sl_; p_last = pl_; cut = ct; t = 26 - pl_;
+        ended = true;
+        return;
+      }
+    }
     t = 26 - P; n = nn; B = BB; sig = sg;
     sig_last = sl;
     p_last = P;
