@@ -185,6 +185,21 @@ WHFF_HD void unroll16(F&& f) {
     unroll16<I + 1>(f);
   }
 }
+// f(0..15) in order, in groups of four; a group (and everything after it)
+// is entered only while `live` has a bit at or above it, so a warp whose
+// lanes have no high coefficients skips the rest of the chain in one branch.
+template <int G = 0, class F>
+WHFF_HD void unroll16_live(uint32_t live, F&& f) {
+  if constexpr (G < 4) {
+    f(std::integral_constant<int, 4 * G>());
+    f(std::integral_constant<int, 4 * G + 1>());
+    f(std::integral_constant<int, 4 * G + 2>());
+    f(std::integral_constant<int, 4 * G + 3>());
+    if constexpr (G < 3) {
+      if (live >> (4 * G + 4)) unroll16_live<G + 1>(live, f);
+    }
+  }
+}
 WHFF_HD uint32_t top_mask(int nbits) {  // top nbits set, nbits in [0, 32]
   return nbits <= 0 ? 0u : (nbits >= 32 ? 0xFFFFFFFFu : ~(0xFFFFFFFFu >> nbits));
 }

@@ -552,7 +552,7 @@ WHFF_HD void decode_block_sf(BitWin& bw, int planes_limit, Decoded& d, Sink&& si
 #else
   for (int i = 0; i < 4; ++i) pv[i] = psw[i];
 #endif
-  unroll16([&](auto cc) {
+  unroll16_live(sig, [&](auto cc) {
     constexpr int c = decltype(cc)::value;
     if ((sig >> c) & 1u) {                   // skipped when no lane of the warp has it
       const uint32_t pb = pv[c >> 2] >> (8 * (c & 3));
