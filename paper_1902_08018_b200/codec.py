@@ -412,6 +412,49 @@ def codec_metrics(original, decoded, stream):
 
 
 # ---------------------------------------------------------------------------
+# block-row shards (a rank uploads only its rows)
+# ---------------------------------------------------------------------------
+
+def shard_rows(stream, row_begin, row_end):
+    """The stream of rows [row_begin, row_end) of `stream`, cut out of its
+    payload without decoding.  Blocks are independent and stored row-major
+    over (block-row, block-col) (codec.py:157-164), so a block-row range is
+    one contiguous bit range; the result is byte-identical to compressing the
+    row window itself (tests/test_shard_rows.py).  row_begin must be a
+    multiple of 4, row_end a multiple of 4 or the stream's last row."""
+    if isinstance(stream, DeviceStream):
+        stream = stream.to_host()
+    rows, cols = stream.rows, stream.cols
+    if not (0 <= row_begin < row_end <= rows):
+        raise DimensionError(f"row range [{row_begin}, {row_end}) outside [0, {rows})")
+    if row_begin % BLOCK or (row_end % BLOCK and row_end != rows):
+        raise DimensionError("shard rows must start (and end, except at the last row) on a "
+                             "block-row boundary (multiples of 4)")
+    bc = (cols + BLOCK - 1) // BLOCK
+    b0 = (row_begin // BLOCK) * bc
+    b1 = ((row_end + BLOCK - 1) // BLOCK) * bc
+    index = np.asarray(stream.block_index, dtype=np.uint64)
+    start = int(index[b0])
+    end = int(index[b1]) if b1 < index.size else int(stream.total_bits)
+    nbits = end - start
+    nbytes = (nbits + 7) // 8
+    src = np.asarray(stream.payload, dtype=np.uint8)
+    lo = start // 8
+    sh = start % 8
+    chunk = np.zeros(nbytes + 1, dtype=np.uint16)
+    take = src[lo: lo + nbytes + 1]
+    chunk[:take.size] = take
+    out = ((chunk[:-1] << sh) | (chunk[1:] >> (8 - sh))).astype(np.uint8) if sh else \
+        chunk[:-1].astype(np.uint8)
+    if nbits % 8:                            # the encoder pads the last byte with zeros
+        out[-1] &= np.uint8((0xFF << (8 - nbits % 8)) & 0xFF)
+    return CompressedStream(mode=stream.mode, rows=row_end - row_begin, cols=cols, payload=out,
+                            block_index=index[b0:b1] - np.uint64(start), total_bits=nbits,
+                            block_size=stream.block_size, version=stream.version,
+                            exact_bits=stream.exact_bits)
+
+
+# ---------------------------------------------------------------------------
 # WHFZ container (SPEC.md:288; codec.py:388-450)
 # ---------------------------------------------------------------------------
 
