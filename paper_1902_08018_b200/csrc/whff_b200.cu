@@ -537,8 +537,8 @@ __global__ void WHFF_GEMV_LB k_decode_gemv(JobTable T, unsigned long long* statu
       if (bn < bc) nxt = ldg(seg128 + row_block0 + bn);   // prefetch this warp's next group
       fb_len = active ? clamp_len(b * 128ull, 128ull, s.payload_bits) : 0;
       win_128(bw, q.x, q.y, q.z, q.w, fb_len);
-      if (kSink) decode_block_sf<false, false, CoefSink&, false>(bw, pl, d, cs);
-      else if (SF) decode_block_sf<false, false>(bw, pl, d);
+      if (kSink) decode_block_sf<false, false, CoefSink&, false, false>(bw, pl, d, cs);
+      else if (SF) decode_block_sf<false, false, NullSink, true, false>(bw, pl, d);
       else decode_block<false, false, false>(bw, pl, d, 0xFFFFFFFFu);
     } else {
       const uint64_t start = pf.start;

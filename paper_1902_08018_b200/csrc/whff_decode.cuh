@@ -188,7 +188,7 @@ WHFF_HD void unroll16(F&& f) {
 // f(0..15) in order, in groups of four; a group (and everything after it)
 // is entered only while `live` has a bit at or above it, so a warp whose
 // lanes have no high coefficients skips the rest of the chain in one branch.
-template <int G = 0, class F>
+template <int G = 0, bool GROUPED = true, class F>
 WHFF_HD void unroll16_live(uint32_t live, F&& f) {
   if constexpr (G < 4) {
     f(std::integral_constant<int, 4 * G>());
@@ -196,7 +196,7 @@ WHFF_HD void unroll16_live(uint32_t live, F&& f) {
     f(std::integral_constant<int, 4 * G + 2>());
     f(std::integral_constant<int, 4 * G + 3>());
     if constexpr (G < 3) {
-      if (live >> (4 * G + 4)) unroll16_live<G + 1>(live, f);
+      if (!GROUPED || (live >> (4 * G + 4))) unroll16_live<G + 1, GROUPED>(live, f);
     }
   }
 }

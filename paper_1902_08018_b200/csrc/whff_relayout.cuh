@@ -489,7 +489,10 @@ struct NullSink {
 
 // MAGS = false: only the sink sees the magnitudes (d.mag is left unset, and
 // so are raw-escape words: the caller re-decodes such blocks with MAGS).
-template <bool HAS_RAW, bool REFILL, class Sink = NullSink, bool MAGS = true>
+// GROUPED: the fields loop leaves the coefficient chain once no lane has
+// higher coefficients (a win for sparse blocks: accuracy / precision modes;
+// FixedRate(8) blocks are dense enough that the extra branches cost ~0.5 %).
+template <bool HAS_RAW, bool REFILL, class Sink = NullSink, bool MAGS = true, bool GROUPED = true>
 WHFF_HD void decode_block_sf(BitWin& bw, int planes_limit, Decoded& d, Sink&& sink = Sink()) {
   const int len = bw.len;
   d.negm = 0;
@@ -552,7 +555,7 @@ WHFF_HD void decode_block_sf(BitWin& bw, int planes_limit, Decoded& d, Sink&& si
 #else
   for (int i = 0; i < 4; ++i) pv[i] = psw[i];
 #endif
-  unroll16_live(sig, [&](auto cc) {
+  unroll16_live<0, GROUPED>(sig, [&](auto cc) {
     constexpr int c = decltype(cc)::value;
     if ((sig >> c) & 1u) {                   // skipped when no lane of the warp has it
       const uint32_t pb = pv[c >> 2] >> (8 * (c & 3));
