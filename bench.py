@@ -191,8 +191,14 @@ def build_field(args, world, rank):
                    torch.from_numpy(fps[(0, 0)]).cuda(), dose, policy=args.policy,
                    evaluation=args.evaluation, world=world, rank=rank,
                    vector_mode=args.vector_mode)
-    stream_bytes = sum(ds.payload_bytes + ds.index_bytes
-                       for row in streams for ds in row if ds is not None)
+    # compressed bytes this rank decodes per step: the block-rows of its jobs
+    # (a slit split across two ranks is held by both but decoded once)
+    stream_bytes = 0
+    for a, s_, r0, r1 in jobs:
+        ds = streams[a][s_]
+        nbr = (r1 + 3) // 4 - r0 // 4
+        stream_bytes += (ds.payload_bytes + ds.index_bytes) * nbr / ds.block_rows
+    stream_bytes = int(round(stream_bytes))
     info = {"t_ops_s": round(t_ops, 2), "t_encode_s": round(t_enc, 2),
             "streams": sum(1 for row in streams for ds in row if ds is not None),
             "distinct_per_axis": distinct, "stream_bytes_rank": stream_bytes,
