@@ -495,6 +495,7 @@ def b200_main(args, world, rank, local):
     value = job_bytes * args.steps / steps_s / 1e9
     achieved = kernel_bytes / (kernel_ms / 1e3) / 1e9
     traffic = None
+    instr = None
     try:
         with open(os.path.join(ROOT, "profiles", "ncu_traffic.json")) as fh:
             tj = json.load(fh)
@@ -503,6 +504,15 @@ def b200_main(args, world, rank, local):
                     and e.get("layout", "reference") == args.layout
                     and e.get("slits", 52) == args.slits and e.get("S", 256000) == args.S):
                 traffic = e.get("dram_bytes_per_launch")
+                if "thread_instr_per_block" in e:
+                    # instruction roofline: the SM issue budget per 16-byte
+                    # block at HBM speed is 128 lane-instr/clk * clk / (blocks/s at peak)
+                    budget = 128 * 148 * 1.965e9 / (hbm * 1e9 / 16)
+                    instr = {"thread_instr_per_block": e["thread_instr_per_block"],
+                             "budget_at_hbm_peak": round(budget, 1),
+                             "alu_pipe_pct": e.get("alu_pipe_pct"),
+                             "issue_active_pct": e.get("issue_active_pct"),
+                             "source": "ncu --set full (profiles/r1_ncu_summary.md)"}
     except Exception:
         pass
     p50 = statistics.median(lat_ms)
@@ -538,7 +548,8 @@ def b200_main(args, world, rank, local):
                      "peak": hbm, "peak_kind": f"{pk_kind} hbm_gbs (burst copy)", "unit": "GB/s",
                      "frac": round(achieved / hbm, 4), "traffic": traffic,
                      "bytes_per_launch": int(kernel_bytes), "kernel_ms": round(kernel_ms, 4),
-                     "share_of_step": round(kernel_ms / (total_ms / args.steps), 3)},
+                     "share_of_step": round(kernel_ms / (total_ms / args.steps), 3),
+                     "instruction_roofline": instr},
         "cpu_baseline": cpu,
         "clocks": clk,
         "setup": info,
