@@ -60,7 +60,7 @@ class PipelineConfig:
     decode_time_override: float = None
     decode_stall_s: dict = field(default_factory=dict)
     # B200 additions
-    evaluation: str = "coefficient"            # "reference" | "exact" | "coefficient"
+    evaluation: str = "exact"                  # "reference" | "exact" | "coefficient"
     policy: str = "mixed"
     layout: str = "skeleton-first"
     step_period_s: float = None                # pace steps on the device clock

@@ -178,3 +178,56 @@ def test_skeleton_first_layout_identical(orc, mode_kind, param, rng):
     assert np.array_equal(back.block_index, host.block_index)
     sf.relayout("reference")
     assert torch.equal(ref.decode(), sf.decode())
+
+
+def coefficient_bound(orc, s, C, v):
+    """Error bound of the coefficient-domain evaluation: it applies the real
+    inverse lift G to the block's coefficients instead of the integer lift, so
+    each block contributes up to K quantisation steps 2^(e-26) per row times
+    sum_j |v_j| over its columns (K = 16 covers the two lift passes' floors),
+    on top of the reference's (W+1) 2^-24 sum|C v|."""
+    mode = mode_of(s)
+    seg = orc.segment_lengths(mode, s.payload.size, s.block_index)
+    mag, neg, emax, raw, rw, _ = orc.decode_blocks(s.payload, s.block_index, seg, 27,
+                                                   orc.planes_limit_for(mode), mode[0] == "accuracy")
+    rows, cols = C.shape
+    bc = (cols + 3) // 4
+    vb = np.zeros(bc * 4)
+    vb[:cols] = np.abs(v.astype(np.float64))
+    vsum = vb.reshape(bc, 4).sum(1)
+    step = np.where((emax > 0) & (raw == 0), np.ldexp(1.0, emax.astype(np.int64) - 160 - 26), 0.0)
+    per_brow = (16 * step.reshape(-1, bc) * vsum[None, :]).sum(1)
+    return bound(C, v) + np.repeat(per_brow, 4)[:rows]
+
+
+def mode_of(s):
+    m = s.mode
+    kind = {"FixedRate": "rate", "FixedPrecision": "precision", "FixedAccuracy": "accuracy"}[type(m).__name__]
+    return (kind, m.bpv if kind == "rate" else m.planes if kind == "precision" else m.tolerance)
+
+
+@pytest.mark.parametrize("evaluation", ["exact", "coefficient"])
+def test_skeleton_first_all_golden_streams(golden, orc, evaluation, rng):
+    """The bench's layout on every golden stream of the reference (ragged
+    shapes, raw escapes, zero blocks, extreme and subnormal scales -- the
+    coefficient kernel's out-of-line exact fallback).  Exact: within the
+    reference's bound; coefficient: within its own (documented) bound, which
+    equals the reference's for blocks without a large intra-block dynamic
+    range (the smooth WHFF operators) and is looser for adversarial ones."""
+    import torch
+    from paper_1902_08018_b200 import codec
+    for case in golden_codec_cases(golden("codec_cases")):
+        if not case["ok"]:
+            continue
+        s = host_stream(case)
+        C = orc.decompress(s)
+        v = rng.standard_normal(C.shape[1]).astype(np.float32)
+        ref = orc.gemv_kernel(C, v, "mixed", "sequential")
+        ds = codec.DeviceStream.from_host(s).relayout("skeleton-first")
+        got = ds.gemv(torch.from_numpy(v).cuda(), evaluation=evaluation).cpu().numpy()
+        ds.close()
+        if evaluation == "exact":
+            check(got, ref, C, v, min_identical=0.9)
+        else:
+            err = np.abs(got.astype(np.float64) - ref.astype(np.float64))
+            assert (err <= coefficient_bound(orc, s, C, v) + 1e-300).all(), case["name"]
