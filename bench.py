@@ -271,6 +271,16 @@ def make_cpu_samples(args, tmpdir):
     return paths
 
 
+def cpu_model():
+    try:
+        for line in open("/proc/cpuinfo"):
+            if line.startswith("model name"):
+                return line.split(":", 1)[1].strip()
+    except OSError:
+        pass
+    return None
+
+
 def run_cpu_leg(paths, reps, warmup=0):
     """Run the CPU path over `reps` x samples with all host cores; returns
     (GB/s compressed, seconds, cores, kind, per-sample seconds)."""
@@ -476,10 +486,13 @@ def b200_main(args, world, rank, local):
         cores = len(os.sched_getaffinity(0)) if hasattr(os, "sched_getaffinity") else os.cpu_count()
         reps = max(1, (5 * cores) // 6)          # ~2.5 chunks per core: 10-30 core-seconds
         v, wall, cores, kind, per, _ = run_cpu_leg(paths, reps)
+        pb = [int(np.load(pth)["payload"].size) for pth in paths]
         cpu = {"value": round(v, 6), "unit": "GB/s", "cores": cores, "kind": kind,
+               "value_1core": round(statistics.mean(pb) / per / 1e9, 6),
+               "cpu_model": cpu_model(),
                "sample": f"{3 * reps} chunks of {args.rows}x{args.cpu_sample_cols} "
                          f"({args.mode}), reference codec.decompress + mpgemv.gemv(mixed, sequential); "
-                         f"{wall:.1f}s wall"}
+                         f"{wall:.1f}s wall; value_1core: the median chunk on one core"}
 
     if rank != 0:
         if world > 1:
