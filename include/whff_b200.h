@@ -137,6 +137,15 @@ whff_status_t whff_dstream_clone(whff_dstream_t s, whff_dstream_t* out);
 whff_status_t whff_dstream_get_info(whff_dstream_t s, whff_dstream_info_t* info);
 /* Copy payload (payload_bytes) and u64 block bit offsets (n_blocks) back to
  * the host, e.g. for codec.py:388-402 save_stream.  Synchronous.           */
+/* Streaming scan staging (pipeline.py:208-289 stage 1, the paper's transfer
+ * stage): the payload bytes exactly as held on the device (device layout, no
+ * inverse permutation) ...                                                 */
+whff_status_t whff_dstream_export_payload(whff_dstream_t s, uint8_t* host_payload);
+/* ... and their asynchronous re-import into a stream of identical geometry
+ * (fixed-rate, same shape: every slit of a field), so a small ring of device
+ * streams can cycle through a field held in (pinned) host memory.          */
+whff_status_t whff_dstream_import_payload_async(whff_dstream_t s, const uint8_t* host_payload,
+                                                uint64_t bytes, whff_stream_t stream);
 whff_status_t whff_dstream_download(whff_dstream_t s, uint8_t* payload_host,
                                     uint64_t* block_index_host);
 

@@ -219,6 +219,21 @@ class DeviceStream:
         return CompressedStream(mode=self.mode, rows=self.rows, cols=self.cols, payload=payload,
                                 block_index=index, total_bits=int(self.total_bits))
 
+    # -- streaming (device-layout payload to / from host memory) ------------
+    def export_payload(self, pinned=True):
+        """The payload exactly as held on the device (device layout), as a
+        (pinned) host uint8 tensor: the staging form of the streaming scan."""
+        import torch
+        out = torch.empty(self.payload_bytes, dtype=torch.uint8, pin_memory=pinned)
+        _lib.call("whff_dstream_export_payload", self._h, _lib.ptr(out))
+        return out
+
+    def import_payload_async(self, host_payload):
+        """Overwrite the payload with a same-geometry stream's exported bytes
+        (async H2D on the current stream when host_payload is pinned)."""
+        _lib.call("whff_dstream_import_payload_async", self._h, _lib.ptr(host_payload),
+                  int(host_payload.numel()), _lib.cur_stream())
+
     # -- device operations -------------------------------------------------
     def decode(self, out=None, check=True):
         """Bit-exact binary32 words as a (rows, cols) CUDA tensor."""

@@ -1270,6 +1270,25 @@ whff_status_t whff_dstream_get_info(whff_dstream_t s, whff_dstream_info_t* info)
   return WHFF_OK;
 }
 
+whff_status_t whff_dstream_export_payload(whff_dstream_t s, uint8_t* host_payload) {
+  if (!s || !host_payload) return fail(WHFF_ERR_ARGUMENT, "null argument");
+  DeviceGuard g(s->device);
+  if (s->payload_bytes) WCK(cudaMemcpy(host_payload, s->d_payload, s->payload_bytes, cudaMemcpyDeviceToHost));
+  return WHFF_OK;
+}
+
+whff_status_t whff_dstream_import_payload_async(whff_dstream_t s, const uint8_t* host_payload,
+                                                uint64_t bytes, whff_stream_t stream) {
+  if (!s || !host_payload) return fail(WHFF_ERR_ARGUMENT, "null argument");
+  if (s->kind != WHFF_INDEX_IMPLICIT)
+    return fail(WHFF_ERR_ARGUMENT, "payload import needs an implicit-index (fixed-rate) stream");
+  if (bytes != s->payload_bytes)
+    return fail(WHFF_ERR_DIMENSION, "imported payload size differs from the stream's geometry");
+  DeviceGuard g(s->device);
+  WCK(cudaMemcpyAsync(s->d_payload, host_payload, bytes, cudaMemcpyHostToDevice, (cudaStream_t)stream));
+  return WHFF_OK;
+}
+
 whff_status_t whff_dstream_download(whff_dstream_t s, uint8_t* payload, uint64_t* index) {
   if (!s) return fail(WHFF_ERR_ARGUMENT, "null stream");
   DeviceGuard g(s->device);

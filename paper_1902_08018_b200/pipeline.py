@@ -21,6 +21,12 @@ What changes:
     ``step_period_s`` set, each schedule step is held until its millisecond
     on the device clock (%globaltimer, whff_wait_until), so the trace is a
     real-time run; without it steps run back to back (throughput mode);
+  * ``streaming=True`` reproduces the reference's stage 1 for fields larger
+    than HBM: the slits' compressed (device-layout) payloads live in pinned
+    host memory and a ring of ``queue_depth`` device slots is refilled by
+    H2D copies on a second CUDA stream, bounded by the consumer exactly like
+    the reference's queue (pipeline.py:225-238); the trace then carries the
+    measured transfer times;
   * a field's latency is its last delivery (end of its last light step)
     minus the field's start, judged against its budget as the reference's
     simulated clock does (pipeline.py:269-270, 285-289).
@@ -64,6 +70,8 @@ class PipelineConfig:
     policy: str = "mixed"
     layout: str = "skeleton-first"
     step_period_s: float = None                # pace steps on the device clock
+    streaming: bool = False                    # stage 1 = H2D of the slit streams (ring of
+                                               # queue_depth device slots; fixed-rate modes)
 
     def __post_init__(self):
         if self.interconnect_bandwidth <= 0:
@@ -81,6 +89,10 @@ class PipelineConfig:
             raise WhffError("step_period_s must be positive")
         if self.codec_mode is None:
             self.codec_mode = codec_mod.FixedAccuracy(1e-12)
+        if self.streaming and not (self.use_compression
+                                   and isinstance(self.codec_mode, codec_mod.FixedRate)):
+            raise WhffError("streaming needs use_compression with a FixedRate codec mode "
+                            "(every slit stream of a field has the same geometry)")
 
 
 @dataclass
@@ -133,11 +145,12 @@ class DeadlineReport:
 # ---------------------------------------------------------------------------
 
 class _Slit:
-    """One (field, slit): the three axis operators on the device."""
+    """One (field, slit): the three axis operators on the device (streaming:
+    their device-layout payloads in pinned host memory instead)."""
 
-    def __init__(self, model, f, s, cfg, dev):
+    def __init__(self, model, f, s, cfg, dev, keep_template=False):
         import torch
-        self.streams, self.mats = [], []
+        self.streams, self.mats, self.host = [], [], []
         self.nbytes = 0
         for axis in AXES:
             if hasattr(model, "slit_rows"):
@@ -150,7 +163,14 @@ class _Slit:
                 self.nbytes += ds.payload_bytes
                 if cfg.evaluation != "reference" and cfg.layout != "reference":
                     ds.relayout(cfg.layout)
-                self.streams.append(ds)
+                if cfg.streaming:
+                    self.host.append(ds.export_payload(pinned=True))
+                    if keep_template:
+                        self.streams.append(ds)
+                    else:
+                        ds.close()
+                else:
+                    self.streams.append(ds)
             else:
                 m = rows if isinstance(rows, torch.Tensor) else torch.from_numpy(
                     np.ascontiguousarray(rows))
@@ -166,7 +186,8 @@ def _prepare(model, schedule, cfg, dev):
         n_slits = model.n_slits(fs.field_id)
         for i in range(fs.t_l):
             need.setdefault((fs.field_id, fs.slit_for_light_step(i, n_slits)), None)
-    return {key: _Slit(model, key[0], key[1], cfg, dev) for key in need}
+    return {key: _Slit(model, key[0], key[1], cfg, dev, keep_template=(i == 0))
+            for i, key in enumerate(need)}
 
 
 # ---------------------------------------------------------------------------
@@ -216,6 +237,14 @@ def run_scan(model, schedule, heatload, cfg=None, resampler=None, backend=None):
     D = torch.zeros((max(n_light, 1), 3, M), dtype=torch.float32, device=dev)
     status = _lib.status_word(dev)
 
+    # streaming: a ring of queue_depth slots, each three device streams of the
+    # field's geometry, refilled by H2D copies on their own CUDA stream
+    ring = None
+    light_keys = [(fs.field_id, slit) for fs, i, phase, slit in steps if phase == "light"]
+    if cfg.streaming:
+        template = next(sl for sl in slits.values() if sl.streams)
+        ring = [[template.streams[a].clone() for a in range(3)] for _ in range(cfg.queue_depth)]
+
     # one plan per light item: the slit's three streams -> D[item, axis]
     plans, scratch = [], None
     item = 0
@@ -224,7 +253,8 @@ def run_scan(model, schedule, heatload, cfg=None, resampler=None, backend=None):
             continue
         sl = slits[(fs.field_id, slit)]
         if cfg.use_compression and cfg.evaluation != "reference":
-            plans.append(GemvPlan([(sl.streams[a], S, D[item, a], 0, M) for a in range(3)],
+            src = ring[item % cfg.queue_depth] if cfg.streaming else sl.streams
+            plans.append(GemvPlan([(src[a], S, D[item, a], 0, M) for a in range(3)],
                                   cfg.policy, cfg.evaluation))
         else:
             plans.append(None)
@@ -240,9 +270,28 @@ def run_scan(model, schedule, heatload, cfg=None, resampler=None, backend=None):
     t_base = torch.zeros(1, dtype=torch.int64, device=dev)
     period_ns = None if cfg.step_period_s is None else int(round(cfg.step_period_s * 1e9))
 
+    cstream = torch.cuda.Stream(dev) if cfg.streaming else None
+    up_s = [torch.cuda.Event(enable_timing=True) for _ in range(n_light)] if cfg.streaming else []
+    up_e = [torch.cuda.Event(enable_timing=True) for _ in range(n_light)] if cfg.streaming else []
+    done = [torch.cuda.Event() for _ in range(n_light)] if cfg.streaming else []
+
+    def upload(it):                          # stage 1 of light item `it` (copy stream)
+        slot = ring[it % cfg.queue_depth]
+        with torch.cuda.stream(cstream):
+            if it >= cfg.queue_depth:        # the slot's previous item has been consumed
+                cstream.wait_event(done[it - cfg.queue_depth])
+            up_s[it].record(cstream)
+            for a in range(3):
+                slot[a].import_payload_async(slits[light_keys[it]].host[a])
+            up_e[it].record(cstream)
+
     status.fill_(-1)
     torch.cuda.synchronize(dev)
     ev0.record(cur)
+    if cfg.streaming:
+        cstream.wait_event(ev0)
+        for it in range(min(cfg.queue_depth, n_light)):
+            upload(it)
     if period_ns is not None:
         _lib.call("whff_device_timestamp", _lib.ptr(t_base), _lib.cur_stream())
     item = 0
@@ -264,7 +313,13 @@ def run_scan(model, schedule, heatload, cfg=None, resampler=None, backend=None):
                     sl.streams[a].decode(out=scratch, check=False)
                     gemv_device(scratch, S, "mixed", "sequential", out=D[item, a])
             else:
+                if cfg.streaming:
+                    cur.wait_event(up_e[item])
                 plans[item].launch(status)
+                if cfg.streaming:
+                    done[item].record(cur)
+                    if item + cfg.queue_depth < n_light:
+                        upload(item + cfg.queue_depth)
             item += 1
         ev_e[j].record(cur)
     torch.cuda.synchronize(dev)
@@ -274,9 +329,12 @@ def run_scan(model, schedule, heatload, cfg=None, resampler=None, backend=None):
     # ---- trace (seconds since the scan started, device clock) ---------------
     t_s = [ev0.elapsed_time(e) / 1e3 for e in ev_s]
     t_e = [ev0.elapsed_time(e) / 1e3 for e in ev_e]
+    t_up = [(ev0.elapsed_time(up_s[i]) / 1e3, ev0.elapsed_time(up_e[i]) / 1e3)
+            for i in range(n_light)] if cfg.streaming else []
     records, fields = [], []
     k = 0
     j = 0
+    li = 0
     for fs in schedule.fields:
         nsteps = fs.t_l + fs.t_d
         field_start = t_s[j]
@@ -285,8 +343,14 @@ def run_scan(model, schedule, heatload, cfg=None, resampler=None, backend=None):
             _, i, phase, slit = steps[j]
             k += 1
             nbytes = slits[(fs.field_id, slit)].nbytes if phase == "light" else 0
-            records.append(StepRecord(fs.field_id, k, phase, slit, nbytes, 0.0, 0.0,
-                                      t_e[j] - t_s[j], t_s[j], t_s[j], t_s[j], t_e[j]))
+            if phase == "light" and cfg.streaming:
+                s1, e1 = t_up[li]
+                records.append(StepRecord(fs.field_id, k, phase, slit, nbytes, e1 - s1, 0.0,
+                                          t_e[j] - t_s[j], s1, e1, t_s[j], t_e[j]))
+            else:
+                records.append(StepRecord(fs.field_id, k, phase, slit, nbytes, 0.0, 0.0,
+                                          t_e[j] - t_s[j], t_s[j], t_s[j], t_s[j], t_e[j]))
+            li += phase == "light"
             if phase == "light":             # a delivery (pipeline.py:269-270, 287)
                 last_delivery = t_e[j]
             j += 1
@@ -306,6 +370,10 @@ def run_scan(model, schedule, heatload, cfg=None, resampler=None, backend=None):
     for p in plans:
         if p is not None:
             p.close()
+    if ring is not None:
+        for slot in ring:
+            for ds in slot:
+                ds.close()
     return ScanResult(deformations, PipelineTrace(records, fields))
 
 

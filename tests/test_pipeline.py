@@ -99,3 +99,12 @@ def test_trace_csv_and_deadline_report(tmp_path):
     rep = pipeline.deadline_report(tr)
     assert rep.miss_rate == 0.5 and rep.worst_latency_s == 8.8e-2
     assert pipeline.deadline_report(tr, budgets={0: 1e-4, 1: 1.0}).verdicts[0][1] is False
+
+
+def test_streaming_config_needs_fixed_rate():
+    from paper_1902_08018_b200 import codec
+    with pytest.raises(WhffError):
+        pipeline.PipelineConfig(streaming=True)              # no compression
+    with pytest.raises(WhffError):
+        pipeline.PipelineConfig(streaming=True, use_compression=True)   # FixedAccuracy default
+    pipeline.PipelineConfig(streaming=True, use_compression=True, codec_mode=codec.FixedRate(8))
