@@ -188,3 +188,57 @@ def test_accuracy_bound_property(rng):
         arr = (rng.standard_normal((r, c)) * 10.0 ** rng.integers(-12, 6)).astype(np.float32)
         dec = codec.decompress(codec.compress(arr, codec.FixedAccuracy(tol)))
         assert np.abs(dec.astype(np.float64) - arr.astype(np.float64)).max() <= tol
+
+
+@pytest.mark.parametrize("kind", ["rate", "precision", "accuracy"])
+def test_fuzz_skeleton_first_on_device(orc, rng, kind):
+    """Arbitrary bits through the device relayout + skeleton-first decoder
+    (event walk, closed-form endings, general walker) vs the oracle's
+    decode_blocks: identical arrays, and the inverse layout restores the
+    bytes.  One block-row of nb blocks per trial."""
+    import torch
+    from paper_1902_08018_b200 import codec
+    from paper_1902_08018_b200.errors import CorruptStreamError
+    for trial in range(60):
+        nb = int(rng.integers(1, 80))
+        if kind == "rate":
+            bpv = 8 if trial % 2 == 0 else int(rng.integers(1, 33))   # 8: the 128-bit kernel
+            mode = codec.FixedRate(bpv)
+            lens = np.full(nb, 16 * bpv, np.uint64)
+        else:
+            mode = codec.FixedPrecision(int(rng.integers(1, 28))) if kind == "precision" \
+                else codec.FixedAccuracy(float(rng.choice([0.0, 1e-12])))
+            lens = rng.integers(1, 600, nb).astype(np.uint64)
+        offs = np.concatenate([[0], np.cumsum(lens)[:-1]]).astype(np.uint64)
+        total = int(lens.sum())
+        nbytes = max(1, (total + 7) // 8) + int(kind != "rate")
+        bits = (rng.random(nbytes * 8) < rng.choice([.5, .12, .88])).astype(np.uint8)
+        payload = np.packbits(bits)
+        s = codec.CompressedStream(mode=mode, rows=4, cols=4 * nb, payload=payload,
+                                   block_index=offs, total_bits=total if kind == "rate" else nbytes * 8)
+        mk = (kind, mode.bpv if kind == "rate" else mode.planes if kind == "precision" else mode.tolerance)
+        seg = orc.segment_lengths(mk, payload.size, offs)
+        ref = orc.decode_blocks(payload, offs, seg, 27, orc.planes_limit_for(mk), kind == "accuracy")
+        ds = codec.DeviceStream.from_host(s).relayout("skeleton-first")
+        got = ds.decode_blocks()
+        for a, b in zip(got, ref):
+            a = a.cpu().numpy() if hasattr(a, "cpu") else a
+            assert np.array_equal(a.reshape(b.shape).astype(b.dtype), b), (trial, kind)
+        assert np.array_equal(ds.to_host().payload, payload)
+        # the fused kernels' variants (in-register window, sink-only magnitudes)
+        # on the same bits: identical to the reference-layout products
+        rl = codec.DeviceStream.from_host(s)
+        v = torch.rand(4 * nb, device="cuda")
+        for ev in ("exact", "coefficient"):
+            outs = []
+            for d in (rl, ds):
+                try:
+                    outs.append(d.gemv(v, evaluation=ev).cpu().numpy().view(np.uint32))
+                except CorruptStreamError:
+                    outs.append("corrupt")
+            if isinstance(outs[0], str) or isinstance(outs[1], str):
+                assert isinstance(outs[0], str) and isinstance(outs[1], str), (trial, ev)
+            else:
+                assert np.array_equal(outs[0], outs[1]), (trial, ev)
+        rl.close()
+        ds.close()
