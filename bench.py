@@ -36,6 +36,9 @@ DEADLINE_MS = 50.0
 def parse():
     ap = argparse.ArgumentParser()
     ap.add_argument("--gpus", type=int, default=1)
+    ap.add_argument("--dist-backend", default="nccl", choices=["nccl", "gloo"],
+                    help="gloo: run the N>1 path with several ranks sharing one GPU (a "
+                         "functional check; numbers are not NVLink numbers)")
     ap.add_argument("--steps", type=int, default=20)
     ap.add_argument("--warmup", type=int, default=5)
     ap.add_argument("--impl", default="b200", choices=["b200", "reference"])
@@ -350,10 +353,14 @@ def b200_main(args, world, rank, local):
     import torch
     import torch.distributed as dist
 
-    torch.cuda.set_device(local)
+    dev_index = local % torch.cuda.device_count()     # == local on a multi-GPU box
+    torch.cuda.set_device(dev_index)
     group = None
     if world > 1:
-        dist.init_process_group("nccl", device_id=torch.device("cuda", local))
+        if args.dist_backend == "nccl":
+            dist.init_process_group("nccl", device_id=torch.device("cuda", dev_index))
+        else:   # functional check of the N>1 path with several ranks on one GPU
+            dist.init_process_group("gloo")
     from paper_1902_08018_b200 import _lib
     _lib.lib()
 
@@ -371,7 +378,7 @@ def b200_main(args, world, rank, local):
         else:
             fs.step_local()
         if world > 1:
-            dist.all_gather_into_tensor(fs.gathered, fs.local)
+            fs.gather()
 
     for _ in range(max(3, args.warmup)):
         step()
@@ -379,7 +386,7 @@ def b200_main(args, world, rank, local):
     fs.check()
 
     # ---- timed region: K steps, per-step events -----------------------------
-    clocks = Clocks(local)
+    clocks = Clocks(dev_index)
     ev = [torch.cuda.Event(enable_timing=True) for _ in range(args.steps + 1)]
     if world > 1:
         dist.barrier()
@@ -442,7 +449,7 @@ def b200_main(args, world, rank, local):
             dist.broadcast(fs.S, src=0)
         fs.products()
         if world > 1:
-            dist.all_gather_into_tensor(fs.gathered, fs.local)
+            fs.gather()
             d_host.copy_(fs.gathered, non_blocking=True)
         else:
             d_host.copy_(fs.local, non_blocking=True)
