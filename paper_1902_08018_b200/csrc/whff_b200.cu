@@ -198,21 +198,57 @@ __global__ void __launch_bounds__(128) k_decode_block_words(StreamView s, uint64
 // ---------------------------------------------------------------------------
 // decompress (codec.py:296-314): bit-exact words, non-finite -> status
 // ---------------------------------------------------------------------------
-template <bool HAS_RAW>
-__global__ void __launch_bounds__(128) k_decode_words(StreamView s, float* out, uint64_t ld,
+// One warp per group of 32 consecutive blocks of a block-row (the fused
+// kernel's organisation): the compact index is resolved with one shuffle scan
+// per warp, the in-register window is used whenever every lane's segment fits
+// it, and the layout is a template parameter.
+template <bool HAS_RAW, bool SF>
+__global__ void __launch_bounds__(256) k_decode_words(StreamView s, float* out, uint64_t ld,
                                                       unsigned long long* status) {
-  const uint64_t b = blockIdx.x * (uint64_t)blockDim.x + threadIdx.x;
-  if (b >= s.br * s.bc) return;
-  uint64_t start;
-  int len;
-  block_extent(s, b, start, len);
+  const uint64_t wid = (blockIdx.x * (uint64_t)blockDim.x + threadIdx.x) >> 5;
+  const int lane = threadIdx.x & 31;
+  if (wid >= s.br * s.gpr) return;                   // warp-uniform
+  const uint64_t brow = wid / s.gpr, g = wid - brow * s.gpr;
+  const uint64_t bcol = g * 32 + lane;
+  const bool active = bcol < s.bc;
+  const uint64_t b = brow * s.bc + bcol;
+  uint64_t start = 0;
+  int len = 0;
+  if (s.kind == WHFF_INDEX_COMPACT) {
+    const uint32_t l = active ? (uint32_t)s.lens[b] : 0u;
+    uint32_t incl = l;
+#pragma unroll
+    for (int o = 1; o < 32; o <<= 1) {
+      const uint32_t t = __shfl_up_sync(0xFFFFFFFFu, incl, o);
+      if (lane >= o) incl += t;
+    }
+    start = s.base[brow * s.gpr + g] + (incl - l);
+    if (active) len = clamp_len(start, l, s.payload_bits);
+  } else if (active) {
+    block_extent(s, b, start, len);
+  }
   BitWin bw;
-  win_at(bw, s.words, start, len);
+  if (active) {
+    win_at(bw, s.words, start, len);
+  } else {
+    bw.w0 = bw.w1 = bw.w2 = bw.w3 = 0u;
+    bw.pos = 0;
+    bw.len = 0;
+    bw.avail = 128;
+    bw.src = s.words;
+  }
   Decoded d;
-  decode_any<HAS_RAW>(s, bw, s.planes_limit, d);
+  if (__any_sync(0xFFFFFFFFu, active && !fits_no_refill(start, len))) {
+    if (SF) decode_block_sf<HAS_RAW, true>(bw, s.planes_limit, d);
+    else decode_block<HAS_RAW, true>(bw, s.planes_limit, d, 0xFFFFFFFFu);
+  } else {
+    if (SF) decode_block_sf<HAS_RAW, false>(bw, s.planes_limit, d);
+    else decode_block<HAS_RAW, false>(bw, s.planes_limit, d, 0xFFFFFFFFu);
+  }
+  if (!active) return;
   float x[16];
   reconstruct_words(d, x);
-  const uint64_t r0 = (b / s.bc) * 4, c0 = (b % s.bc) * 4;
+  const uint64_t r0 = brow * 4, c0 = bcol * 4;
   unsigned long long bad = ~0ull;
 #pragma unroll
   for (int i = 0; i < 4; ++i) {
@@ -1510,10 +1546,17 @@ whff_status_t whff_decode(whff_dstream_t s, float* out, uint64_t ld, uint64_t* s
   const StreamView v = s->view();
   cudaStream_t cs = (cudaStream_t)stream;
   auto* st = reinterpret_cast<unsigned long long*>(status);
-  if (s->has_raw)
-    k_decode_words<true><<<grid_for(s->nb, 128), 128, 0, cs>>>(v, out, ld, st);
-  else
-    k_decode_words<false><<<grid_for(s->nb, 128), 128, 0, cs>>>(v, out, ld, st);
+  const uint64_t warps = s->br * s->gpr;
+  if (warps == 0) return WHFF_OK;
+  const unsigned grid = (unsigned)((warps + 7) / 8);
+  const bool sf = s->layout == WHFF_LAYOUT_SKELETON_FIRST;
+  if (s->has_raw) {
+    if (sf) k_decode_words<true, true><<<grid, 256, 0, cs>>>(v, out, ld, st);
+    else k_decode_words<true, false><<<grid, 256, 0, cs>>>(v, out, ld, st);
+  } else {
+    if (sf) k_decode_words<false, true><<<grid, 256, 0, cs>>>(v, out, ld, st);
+    else k_decode_words<false, false><<<grid, 256, 0, cs>>>(v, out, ld, st);
+  }
   WCK_LAUNCH("decode");
   return WHFF_OK;
 }

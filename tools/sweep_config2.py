@@ -24,9 +24,29 @@ v = torch.rand(cols, device="cuda")
 st = _lib.status_word()
 modes = [codec.FixedRate(4), codec.FixedRate(8), codec.FixedRate(16), codec.FixedPrecision(17),
          codec.FixedAccuracy(1e-12)]
+words = torch.empty_like(C)
 for mode in modes:
     ds = codec.compress_device(C, mode)
     ds.relayout("skeleton-first")
+    # decode-only (codec.decompress on the device: bit-exact binary32 words to HBM)
+    for _ in range(2):
+        ds.decode(out=words, check=False)
+    torch.cuda.synchronize()
+    e0, e1 = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
+    e0.record()
+    for _ in range(5):
+        ds.decode(out=words, check=False)
+    e1.record()
+    torch.cuda.synchronize()
+    ms = e0.elapsed_time(e1) / 5
+    comp = ds.payload_bytes + ds.index_bytes
+    print(json.dumps({"config": "configs[1] mid-size sweep", "shape": [rows, cols], "mode": repr(mode),
+                      "evaluation": "decode-only (whff_decode)", "compressed_bytes": comp,
+                      "bpv": round(8 * comp / (rows * cols), 3), "ms": round(ms, 4),
+                      "compressed_gbs": round(comp / ms / 1e6, 1), "gflops": None,
+                      "decoded_gbs": round(4 * rows * cols / ms / 1e6, 1),
+                      "roofline_frac": round((comp + 4 * rows * cols) / ms / 1e6 / peak, 4)}),
+          flush=True)
     for ev in ("coefficient", "exact"):
         y = torch.empty(rows, device="cuda")
         plan = GemvPlan([(ds, v, y, 0, rows)], "mixed", ev)
