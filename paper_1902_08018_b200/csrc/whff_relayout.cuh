@@ -243,7 +243,8 @@ struct SkelWalk {
   // kept as an ordered nibble list, so the hit is nibble (off + z) and
   // removing it is a masked 64-bit merge (no per-coefficient loop).  A token
   // that would cross the budget, the plane limit or the window, or that has
-  // no hit, leaves the loop untouched; run_from() finishes the block with the
+  // no hit, leaves the loop untouched; the closed-form ending below resolves
+  // the usual cases, and run_from() finishes any other block with the
   // general (reference-order) logic from exactly this state.
   WHFF_HD void run_fast(int pl) {
     if (ended) return;
