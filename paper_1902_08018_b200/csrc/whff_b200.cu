@@ -540,6 +540,8 @@ __global__ void WHFF_GEMV_LB k_decode_gemv(JobTable T, unsigned long long* statu
   const uint64_t row_block0 = brow * bc;
   const uint4* __restrict__ seg128 = reinterpret_cast<const uint4*>(s.words);
   uint4 nxt = make_uint4(0, 0, 0, 0);
+  // FixedRate(8): the payload covers this block-row's segments completely
+  const bool row_full = VAR == 0 && (row_block0 + bc) * 128ull <= s.payload_bits;
   if (VAR == 0) {
     const uint64_t bcol0 = (uint64_t)warp * 32 + lane;
     if (bcol0 < bc) nxt = ldg(seg128 + row_block0 + bcol0);
@@ -571,8 +573,13 @@ __global__ void WHFF_GEMV_LB k_decode_gemv(JobTable T, unsigned long long* statu
       const uint4 q = nxt;
       const uint64_t bn = bcol + 32 * kGemvWarps;
       if (bn < bc) nxt = ldg(seg128 + row_block0 + bn);   // prefetch this warp's next group
-      fb_len = active ? clamp_len(b * 128ull, 128ull, s.payload_bits) : 0;
-      win_128(bw, q.x, q.y, q.z, q.w, fb_len);
+      if (row_full) {                        // every segment of the row is whole: no masks
+        fb_len = 128;                        // (lanes past the row end decode zeros, discarded)
+        win_128(bw, q.x, q.y, q.z, q.w, 128);
+      } else {
+        fb_len = active ? clamp_len(b * 128ull, 128ull, s.payload_bits) : 0;
+        win_128(bw, q.x, q.y, q.z, q.w, fb_len);
+      }
       if (kSink) decode_block_sf<false, false, CoefSink&, false, false>(bw, pl, d, cs);
       else if (SF) decode_block_sf<false, false, NullSink, true, false>(bw, pl, d);
       else decode_block<false, false, false>(bw, pl, d, 0xFFFFFFFFu);
