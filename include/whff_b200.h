@@ -138,14 +138,22 @@ whff_status_t whff_dstream_get_info(whff_dstream_t s, whff_dstream_info_t* info)
 /* Copy payload (payload_bytes) and u64 block bit offsets (n_blocks) back to
  * the host, e.g. for codec.py:388-402 save_stream.  Synchronous.           */
 /* Streaming scan staging (pipeline.py:208-289 stage 1, the paper's transfer
- * stage): the payload bytes exactly as held on the device (device layout, no
- * inverse permutation) ...                                                 */
-whff_status_t whff_dstream_export_payload(whff_dstream_t s, uint8_t* host_payload);
-/* ... and their asynchronous re-import into a stream of identical geometry
- * (fixed-rate, same shape: every slit of a field), so a small ring of device
- * streams can cycle through a field held in (pinned) host memory.          */
-whff_status_t whff_dstream_import_payload_async(whff_dstream_t s, const uint8_t* host_payload,
-                                                uint64_t bytes, whff_stream_t stream);
+ * stage).  export: the stream's device-layout payload and index arrays
+ * (compact: base u64[br*gpr] + lens u16[nb]; full: starts u64[nb] + lens
+ * u16[nb]; implicit: none) to host memory -- pass NULL buffers to query the
+ * sizes.  reserve: grow a stream's payload capacity.  import_async: rebind a
+ * slot stream (same rows, cols, mode, index kind; payload within capacity)
+ * to exported contents: its geometry (payload size) changes immediately --
+ * plans created afterwards see it -- and the bytes are copied in `stream`
+ * order (pinned host memory for an asynchronous copy).                     */
+whff_status_t whff_dstream_export(whff_dstream_t s, uint8_t* payload_host, uint64_t* payload_bytes,
+                                  uint8_t* index_host, uint64_t* index_bytes);
+whff_status_t whff_dstream_reserve(whff_dstream_t s, uint64_t payload_capacity);
+/* the geometry part of import_async alone (no copy)                        */
+whff_status_t whff_dstream_rebind(whff_dstream_t s, uint64_t payload_bytes);
+whff_status_t whff_dstream_import_async(whff_dstream_t s, const uint8_t* payload_host,
+                                        uint64_t payload_bytes, const uint8_t* index_host,
+                                        uint64_t index_bytes, whff_stream_t stream);
 whff_status_t whff_dstream_download(whff_dstream_t s, uint8_t* payload_host,
                                     uint64_t* block_index_host);
 

@@ -51,8 +51,10 @@ _SIG = {
     "whff_dstream_relayout": ([_P, _I, _P], _I),
     "whff_dstream_get_info": ([_P, _P], _I),
     "whff_dstream_download": ([_P, _P, _P], _I),
-    "whff_dstream_export_payload": ([_P, _P], _I),
-    "whff_dstream_import_payload_async": ([_P, _P, _U64, _P], _I),
+    "whff_dstream_export": ([_P, _P, _P, _P, _P], _I),
+    "whff_dstream_reserve": ([_P, _U64], _I),
+    "whff_dstream_rebind": ([_P, _U64], _I),
+    "whff_dstream_import_async": ([_P, _P, _U64, _P, _U64, _P], _I),
     "whff_compress": ([_P, _U64, _U64, _U64, _I, ctypes.c_double, _P, _P], _I),
     "whff_encode_blocks_size": ([_P, _P, _P, _P, _P, _P, _U64, _I, _I, _I, _P, _P, _P], _I),
     "whff_encode_blocks_emit": ([_P, _P, _P, _P, _P, _P, _U64, _I, _I, _I, _P, _P, _P], _I),

@@ -219,20 +219,32 @@ class DeviceStream:
         return CompressedStream(mode=self.mode, rows=self.rows, cols=self.cols, payload=payload,
                                 block_index=index, total_bits=int(self.total_bits))
 
-    # -- streaming (device-layout payload to / from host memory) ------------
-    def export_payload(self, pinned=True):
-        """The payload exactly as held on the device (device layout), as a
-        (pinned) host uint8 tensor: the staging form of the streaming scan."""
+    # -- streaming (device-layout contents to / from host memory) -----------
+    def export(self, pinned=True):
+        """(payload, index blob) exactly as held on the device (device layout),
+        as (pinned) host uint8 tensors: the staging form of the streaming scan."""
         import torch
-        out = torch.empty(self.payload_bytes, dtype=torch.uint8, pin_memory=pinned)
-        _lib.call("whff_dstream_export_payload", self._h, _lib.ptr(out))
-        return out
+        pb, ib = ctypes.c_uint64(), ctypes.c_uint64()
+        _lib.call("whff_dstream_export", self._h, None, ctypes.byref(pb), None, ctypes.byref(ib))
+        payload = torch.empty(pb.value, dtype=torch.uint8, pin_memory=pinned)
+        index = torch.empty(ib.value, dtype=torch.uint8, pin_memory=pinned)
+        _lib.call("whff_dstream_export", self._h, _lib.ptr(payload), None, _lib.ptr(index), None)
+        return payload, index
 
-    def import_payload_async(self, host_payload):
-        """Overwrite the payload with a same-geometry stream's exported bytes
-        (async H2D on the current stream when host_payload is pinned)."""
-        _lib.call("whff_dstream_import_payload_async", self._h, _lib.ptr(host_payload),
-                  int(host_payload.numel()), _lib.cur_stream())
+    def reserve(self, payload_capacity):
+        _lib.call("whff_dstream_reserve", self._h, int(payload_capacity))
+
+    def rebind(self, payload_bytes):
+        """Set the payload size alone (for plans built before the bytes arrive)."""
+        _lib.call("whff_dstream_rebind", self._h, int(payload_bytes))
+        self.payload_bytes = int(payload_bytes)
+
+    def import_async(self, payload, index):
+        """Rebind to a same-geometry stream's exported contents (async H2D on
+        the current stream; the payload size changes at once for new plans)."""
+        _lib.call("whff_dstream_import_async", self._h, _lib.ptr(payload), int(payload.numel()),
+                  _lib.ptr(index) if index.numel() else None, int(index.numel()), _lib.cur_stream())
+        self.payload_bytes = int(payload.numel())
 
     # -- device operations -------------------------------------------------
     def decode(self, out=None, check=True):

@@ -1313,22 +1313,78 @@ whff_status_t whff_dstream_get_info(whff_dstream_t s, whff_dstream_info_t* info)
   return WHFF_OK;
 }
 
-whff_status_t whff_dstream_export_payload(whff_dstream_t s, uint8_t* host_payload) {
-  if (!s || !host_payload) return fail(WHFF_ERR_ARGUMENT, "null argument");
+// index arrays of a stream as one blob: compact = base (br*gpr u64) + lens
+// (nb u16); full = starts (nb u64) + lens (nb u16); implicit = nothing
+static uint64_t index_blob_bytes(const whff_dstream* s) {
+  if (s->kind == WHFF_INDEX_COMPACT) return s->br * s->gpr * 8 + s->nb * 2;
+  if (s->kind == WHFF_INDEX_FULL) return s->nb * 8 + s->nb * 2;
+  return 0;
+}
+
+whff_status_t whff_dstream_export(whff_dstream_t s, uint8_t* payload, uint64_t* payload_bytes,
+                                  uint8_t* index, uint64_t* index_bytes) {
+  if (!s) return fail(WHFF_ERR_ARGUMENT, "null stream");
+  if (payload_bytes) *payload_bytes = s->payload_bytes;
+  if (index_bytes) *index_bytes = index_blob_bytes(s);
   DeviceGuard g(s->device);
-  if (s->payload_bytes) WCK(cudaMemcpy(host_payload, s->d_payload, s->payload_bytes, cudaMemcpyDeviceToHost));
+  if (payload && s->payload_bytes)
+    WCK(cudaMemcpy(payload, s->d_payload, s->payload_bytes, cudaMemcpyDeviceToHost));
+  if (index && s->kind != WHFF_INDEX_IMPLICIT) {
+    const uint64_t first = s->kind == WHFF_INDEX_COMPACT ? s->br * s->gpr * 8 : s->nb * 8;
+    WCK(cudaMemcpy(index, s->kind == WHFF_INDEX_COMPACT ? (const void*)s->d_base : (const void*)s->d_starts,
+                   first, cudaMemcpyDeviceToHost));
+    WCK(cudaMemcpy(index + first, s->d_lens, s->nb * 2, cudaMemcpyDeviceToHost));
+  }
   return WHFF_OK;
 }
 
-whff_status_t whff_dstream_import_payload_async(whff_dstream_t s, const uint8_t* host_payload,
-                                                uint64_t bytes, whff_stream_t stream) {
-  if (!s || !host_payload) return fail(WHFF_ERR_ARGUMENT, "null argument");
-  if (s->kind != WHFF_INDEX_IMPLICIT)
-    return fail(WHFF_ERR_ARGUMENT, "payload import needs an implicit-index (fixed-rate) stream");
-  if (bytes != s->payload_bytes)
-    return fail(WHFF_ERR_DIMENSION, "imported payload size differs from the stream's geometry");
+whff_status_t whff_dstream_reserve(whff_dstream_t s, uint64_t payload_capacity) {
+  if (!s) return fail(WHFF_ERR_ARGUMENT, "null stream");
+  const size_t want = ((payload_capacity + 15) / 16) * 16 + 64;
+  if (want <= s->payload_alloc) return WHFF_OK;
   DeviceGuard g(s->device);
-  WCK(cudaMemcpyAsync(s->d_payload, host_payload, bytes, cudaMemcpyHostToDevice, (cudaStream_t)stream));
+  uint8_t* np = nullptr;
+  WCK(cudaMalloc(&np, want));
+  cudaError_t e = cudaMemset(np, 0, want);
+  if (e == cudaSuccess) e = cudaMemcpy(np, s->d_payload, s->payload_bytes, cudaMemcpyDeviceToDevice);
+  if (e != cudaSuccess) { cudaFree(np); return cuda_fail(e, "reserve payload"); }
+  cudaFree(s->d_payload);
+  s->d_payload = np;
+  s->payload_alloc = want;
+  return WHFF_OK;
+}
+
+whff_status_t whff_dstream_rebind(whff_dstream_t s, uint64_t payload_bytes) {
+  if (!s) return fail(WHFF_ERR_ARGUMENT, "null stream");
+  if (((payload_bytes + 15) / 16) * 16 + 64 > s->payload_alloc)
+    return fail(WHFF_ERR_DIMENSION, "payload exceeds the stream's capacity (whff_dstream_reserve)");
+  if (s->kind == WHFF_INDEX_IMPLICIT && payload_bytes != s->payload_bytes)
+    return fail(WHFF_ERR_DIMENSION, "fixed-rate payload size differs from the stream's geometry");
+  s->payload_bytes = payload_bytes;
+  s->payload_bits = payload_bytes * 8;
+  if (s->kind != WHFF_INDEX_IMPLICIT) s->total_bits = s->payload_bits;
+  return WHFF_OK;
+}
+
+whff_status_t whff_dstream_import_async(whff_dstream_t s, const uint8_t* payload, uint64_t payload_bytes,
+                                        const uint8_t* index, uint64_t index_bytes, whff_stream_t stream) {
+  if (!s || (payload_bytes && !payload)) return fail(WHFF_ERR_ARGUMENT, "null argument");
+  if (index_bytes != index_blob_bytes(s))
+    return fail(WHFF_ERR_DIMENSION, "imported index does not match the stream's geometry");
+  if (index_bytes && !index) return fail(WHFF_ERR_ARGUMENT, "null index");
+  // geometry first (host fields: plans created from now on see it) ...
+  whff_status_t st = whff_dstream_rebind(s, payload_bytes);
+  if (st != WHFF_OK) return st;
+  DeviceGuard g(s->device);
+  cudaStream_t cs = (cudaStream_t)stream;
+  // ... then the bytes, in stream order
+  if (payload_bytes) WCK(cudaMemcpyAsync(s->d_payload, payload, payload_bytes, cudaMemcpyHostToDevice, cs));
+  if (index_bytes) {
+    const uint64_t first = s->kind == WHFF_INDEX_COMPACT ? s->br * s->gpr * 8 : s->nb * 8;
+    WCK(cudaMemcpyAsync(s->kind == WHFF_INDEX_COMPACT ? (void*)s->d_base : (void*)s->d_starts, index, first,
+                        cudaMemcpyHostToDevice, cs));
+    WCK(cudaMemcpyAsync(s->d_lens, index + first, s->nb * 2, cudaMemcpyHostToDevice, cs));
+  }
   return WHFF_OK;
 }
 

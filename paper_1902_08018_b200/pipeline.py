@@ -22,9 +22,9 @@ What changes:
     on the device clock (%globaltimer, whff_wait_until), so the trace is a
     real-time run; without it steps run back to back (throughput mode);
   * ``streaming=True`` reproduces the reference's stage 1 for fields larger
-    than HBM: the slits' compressed (device-layout) payloads live in pinned
-    host memory and a ring of ``queue_depth`` device slots is refilled by
-    H2D copies on a second CUDA stream, bounded by the consumer exactly like
+    than HBM: the slits' compressed (device-layout) payloads and index arrays
+    live in pinned host memory and a ring of ``queue_depth`` device slots is
+    refilled by H2D copies on a second CUDA stream, bounded by the consumer exactly like
     the reference's queue (pipeline.py:225-238); the trace then carries the
     measured transfer times;
   * a field's latency is its last delivery (end of its last light step)
@@ -71,7 +71,7 @@ class PipelineConfig:
     layout: str = "skeleton-first"
     step_period_s: float = None                # pace steps on the device clock
     streaming: bool = False                    # stage 1 = H2D of the slit streams (ring of
-                                               # queue_depth device slots; fixed-rate modes)
+                                               # queue_depth device slots)
 
     def __post_init__(self):
         if self.interconnect_bandwidth <= 0:
@@ -89,10 +89,8 @@ class PipelineConfig:
             raise WhffError("step_period_s must be positive")
         if self.codec_mode is None:
             self.codec_mode = codec_mod.FixedAccuracy(1e-12)
-        if self.streaming and not (self.use_compression
-                                   and isinstance(self.codec_mode, codec_mod.FixedRate)):
-            raise WhffError("streaming needs use_compression with a FixedRate codec mode "
-                            "(every slit stream of a field has the same geometry)")
+        if self.streaming and not self.use_compression:
+            raise WhffError("streaming stages compressed slit streams (use_compression=True)")
 
 
 @dataclass
@@ -164,7 +162,7 @@ class _Slit:
                 if cfg.evaluation != "reference" and cfg.layout != "reference":
                     ds.relayout(cfg.layout)
                 if cfg.streaming:
-                    self.host.append(ds.export_payload(pinned=True))
+                    self.host.append(ds.export(pinned=True))
                     if keep_template:
                         self.streams.append(ds)
                     else:
@@ -243,7 +241,11 @@ def run_scan(model, schedule, heatload, cfg=None, resampler=None, backend=None):
     light_keys = [(fs.field_id, slit) for fs, i, phase, slit in steps if phase == "light"]
     if cfg.streaming:
         template = next(sl for sl in slits.values() if sl.streams)
+        cap = [max(int(sl.host[a][0].numel()) for sl in slits.values()) for a in range(3)]
         ring = [[template.streams[a].clone() for a in range(3)] for _ in range(cfg.queue_depth)]
+        for slot in ring:
+            for a in range(3):
+                slot[a].reserve(cap[a])
 
     # one plan per light item: the slit's three streams -> D[item, axis]
     plans, scratch = [], None
@@ -254,6 +256,9 @@ def run_scan(model, schedule, heatload, cfg=None, resampler=None, backend=None):
         sl = slits[(fs.field_id, slit)]
         if cfg.use_compression and cfg.evaluation != "reference":
             src = ring[item % cfg.queue_depth] if cfg.streaming else sl.streams
+            if cfg.streaming:                # the item's payload sizes, for its plan
+                for a in range(3):
+                    src[a].rebind(sl.host[a][0].numel())
             plans.append(GemvPlan([(src[a], S, D[item, a], 0, M) for a in range(3)],
                                   cfg.policy, cfg.evaluation))
         else:
@@ -282,7 +287,7 @@ def run_scan(model, schedule, heatload, cfg=None, resampler=None, backend=None):
                 cstream.wait_event(done[it - cfg.queue_depth])
             up_s[it].record(cstream)
             for a in range(3):
-                slot[a].import_payload_async(slits[light_keys[it]].host[a])
+                slot[a].import_async(*slits[light_keys[it]].host[a])
             up_e[it].record(cstream)
 
     status.fill_(-1)
@@ -305,21 +310,22 @@ def run_scan(model, schedule, heatload, cfg=None, resampler=None, backend=None):
         T, T_next = T_next, T
         if phase == "light":
             sl = slits[(fs.field_id, slit)]
+            if cfg.streaming:                # stage 1 of this item must have landed
+                cur.wait_event(up_e[item])
             if not cfg.use_compression:
                 for a in range(3):
                     gemv_device(sl.mats[a], S, "mixed", "sequential", out=D[item, a])
             elif cfg.evaluation == "reference":
+                src = ring[item % cfg.queue_depth] if cfg.streaming else sl.streams
                 for a in range(3):
-                    sl.streams[a].decode(out=scratch, check=False)
+                    src[a].decode(out=scratch, check=False)
                     gemv_device(scratch, S, "mixed", "sequential", out=D[item, a])
             else:
-                if cfg.streaming:
-                    cur.wait_event(up_e[item])
                 plans[item].launch(status)
-                if cfg.streaming:
-                    done[item].record(cur)
-                    if item + cfg.queue_depth < n_light:
-                        upload(item + cfg.queue_depth)
+            if cfg.streaming:                # release the slot, refill it with item + depth
+                done[item].record(cur)
+                if item + cfg.queue_depth < n_light:
+                    upload(item + cfg.queue_depth)
             item += 1
         ev_e[j].record(cur)
     torch.cuda.synchronize(dev)

@@ -101,10 +101,9 @@ def test_trace_csv_and_deadline_report(tmp_path):
     assert pipeline.deadline_report(tr, budgets={0: 1e-4, 1: 1.0}).verdicts[0][1] is False
 
 
-def test_streaming_config_needs_fixed_rate():
+def test_streaming_config_needs_compression():
     from paper_1902_08018_b200 import codec
     with pytest.raises(WhffError):
-        pipeline.PipelineConfig(streaming=True)              # no compression
-    with pytest.raises(WhffError):
-        pipeline.PipelineConfig(streaming=True, use_compression=True)   # FixedAccuracy default
+        pipeline.PipelineConfig(streaming=True)              # nothing compressed to stage
+    pipeline.PipelineConfig(streaming=True, use_compression=True)
     pipeline.PipelineConfig(streaming=True, use_compression=True, codec_mode=codec.FixedRate(8))

@@ -1,8 +1,8 @@
 """Paper-scale device scan: run_scan over fields of 52 slits
 x 378 x 256,000 per axis (compressed on the GPU), fast schedule (34 light + 36
 dark ms, 50 ms budget), paced at 1 ms per step on the device clock and
-unpaced; slits resident in HBM, and (fixed-rate modes) streamed from pinned
-host memory through a 4-slot ring (the reference's stage 1).  One JSON line.
+unpaced; slits resident in HBM, and streamed from pinned host memory through
+a 4-slot ring (the reference's stage 1).  One JSON line.
 Usage: python tools/scan_bench.py [n_fields] [mode] [evaluation]"""
 import json
 import os
@@ -28,9 +28,8 @@ sched = model.build_scan_schedule("fast", n_fields)
 out = {"workload": f"paper-scale scan: {n_fields} fields x 52 slits x 3 axes x 378x256000, "
                    f"{mode_s}, fast schedule (34 light + 36 dark ms, budget 50 ms)",
        "evaluation": ev, "setup_s": None}
-variants = [("paced_1ms", 1e-3, False), ("unpaced", None, False)]
-if isinstance(mode, codec.FixedRate):
-    variants += [("streaming_paced_1ms", 1e-3, True), ("streaming_unpaced", None, True)]
+variants = [("paced_1ms", 1e-3, False), ("unpaced", None, False),
+            ("streaming_paced_1ms", 1e-3, True), ("streaming_unpaced", None, True)]
 for tag, period, streaming in variants:
     cfg = pipeline.PipelineConfig(use_compression=True, codec_mode=mode, evaluation=ev,
                                   step_period_s=period, streaming=streaming, queue_depth=4)
