@@ -58,7 +58,10 @@ def parse():
     ap.add_argument("--distinct", type=int, default=0,
                     help="distinct slit contents per axis (0 = all); the rest are "
                          "physically distinct HBM copies")
-    ap.add_argument("--vector-mode", default="broadcast", choices=["broadcast", "replicate"])
+    ap.add_argument("--vector-mode", default="replicate", choices=["broadcast", "replicate"],
+                    help="replicate: every rank runs the deterministic thermal step (~25 MB), "
+                         "so the step needs no broadcast and stays CUDA-graph captured; "
+                         "broadcast: rank 0 computes S and broadcasts it")
     ap.add_argument("--no-cpu-baseline", action="store_true")
     ap.add_argument("--cpu-sample-cols", type=int, default=8192)
     ap.add_argument("--no-graph", action="store_true")
