@@ -59,7 +59,9 @@ class PipelineConfig:
     decode_throughput: float = 33e9
     queue_depth: int = 2
     axis_workers: int = 1
-    time_source: str = "device"
+    time_source: str = "device"                # "device" (= "real"): CUDA events /
+                                               # %globaltimer; "simulated": the reference's
+                                               # cost-model clock (pipeline.py:208-289)
     compute_flops_per_s: float = 50e9
     transfer_time_override: float = None
     compute_time_override: float = None
@@ -80,9 +82,8 @@ class PipelineConfig:
             raise WhffError("queue_depth must be >= 2 (double buffering)")
         if not 1 <= self.axis_workers <= 3:
             raise WhffError("axis_workers must be in 1..3")
-        if self.time_source != "device":
-            raise WhffError(f"time source {self.time_source!r}: the B200 pipeline measures on "
-                            "the device (time_source='device')")
+        if self.time_source not in ("device", "real", "simulated"):
+            raise WhffError(f"unknown time source {self.time_source!r}")
         if self.evaluation not in ("reference", "exact", "coefficient"):
             raise WhffError(f"unknown evaluation {self.evaluation!r}")
         if self.step_period_s is not None and self.step_period_s <= 0:
@@ -150,6 +151,7 @@ class _Slit:
         import torch
         self.streams, self.mats, self.host = [], [], []
         self.nbytes = 0
+        self.raw_bytes = 3 * model.spec.M * model.S * 4    # sum of c_slit.nbytes
         for axis in AXES:
             if hasattr(model, "slit_rows"):
                 rows = model.slit_rows(axis, f, s, device=dev)
@@ -365,6 +367,9 @@ def run_scan(model, schedule, heatload, cfg=None, resampler=None, backend=None):
         fields.append(FieldRecord(fs.field_id, field_start, t_e[j - 1], latency, budget,
                                   latency <= budget))
 
+    if cfg.time_source == "simulated":       # the reference's clock, same values
+        records, fields = _simulated_trace(model, schedule, cfg, slits)
+
     Dh = D[:n_light].cpu().numpy()
     deformations = {}
     for a, axis in enumerate(AXES):
@@ -381,6 +386,98 @@ def run_scan(model, schedule, heatload, cfg=None, resampler=None, backend=None):
             for ds in slot:
                 ds.close()
     return ScanResult(deformations, PipelineTrace(records, fields))
+
+
+# ---------------------------------------------------------------------------
+# the reference's simulated clock (pipeline.py:155-162, 184-196, 208-289)
+# ---------------------------------------------------------------------------
+
+def _step_flops(model, light):
+    """pipeline.py:155-162: sparse update + diagonal input + interpolation,
+    plus the three per-axis products on light steps."""
+    flops = 2 * model.A.nnz + 2 * model.T + 2 * model.P.nnz
+    if light:
+        flops += 3 * model.spec.M * (2 * model.S - 1)
+    return flops
+
+
+def _stage1_times(cfg, field_id, nbytes, raw_bytes):
+    """pipeline.py:184-196."""
+    if cfg.transfer_time_override is not None:
+        t_transfer = cfg.transfer_time_override
+    else:
+        t_transfer = nbytes / cfg.interconnect_bandwidth
+    if cfg.decode_time_override is not None:
+        t_decode = cfg.decode_time_override
+    elif cfg.use_compression:
+        t_decode = raw_bytes / cfg.decode_throughput
+    else:
+        t_decode = 0.0
+    t_decode += cfg.decode_stall_s.get(field_id, 0.0)
+    return t_transfer, t_decode
+
+
+def _simulated_trace(model, schedule, cfg, slits):
+    """The trace of the reference's simulated two-stage pipeline
+    (pipeline.py:208-289): a producer that may run queue_depth light items
+    ahead of the consumer, consumer steps costed by the flop model.  Pure host
+    arithmetic over the deterministic step list, evaluated in the reference's
+    order so the times are identical."""
+    items = []
+    for fs in schedule.fields:
+        n_slits = model.n_slits(fs.field_id)
+        for i in range(fs.t_l):
+            slit = fs.slit_for_light_step(i, n_slits)
+            sl = slits[(fs.field_id, slit)]
+            items.append((slit, sl.nbytes) + _stage1_times(cfg, fs.field_id, sl.nbytes,
+                                                           sl.raw_bytes))
+    p_finish, c_start = [], []
+    last = [0.0]
+
+    def produce_through(i):
+        while len(p_finish) <= i:
+            j = len(p_finish)
+            start = last[0]
+            if j >= cfg.queue_depth:         # bounded queue
+                start = max(start, c_start[j - cfg.queue_depth])
+            last[0] = start + items[j][2] + items[j][3]
+            p_finish.append((start, last[0]))
+
+    steps, fields = [], []
+    c_time, item, k = 0.0, 0, 0
+    for fs in schedule.fields:
+        field_start = c_time
+        last_delivery = c_time
+        for i in range(fs.t_l + fs.t_d):
+            k += 1
+            light = i < fs.t_l
+            if cfg.compute_time_override is not None:
+                t_comp = cfg.compute_time_override
+            else:
+                t_comp = _step_flops(model, light) / cfg.compute_flops_per_s
+                if light:
+                    t_comp /= min(cfg.axis_workers, 3)
+            if light:
+                produce_through(item)
+                slit, nbytes, t_tr, t_dec = items[item]
+                s1_start, s1_end = p_finish[item]
+                s2_start = max(c_time, s1_end)
+                c_start.append(s2_start)
+                s2_end = s2_start + t_comp
+                steps.append(StepRecord(fs.field_id, k, "light", slit, nbytes, t_tr, t_dec, t_comp,
+                                        s1_start, s1_end, s2_start, s2_end))
+                last_delivery = s2_end
+                item += 1
+            else:
+                s2_start, s2_end = c_time, c_time + t_comp
+                steps.append(StepRecord(fs.field_id, k, "dark", -1, 0, 0.0, 0.0, t_comp,
+                                        s2_start, s2_start, s2_start, s2_end))
+            c_time = s2_end
+        latency = last_delivery - field_start
+        budget = fs.time_budget_ms / 1e3
+        fields.append(FieldRecord(fs.field_id, field_start, c_time, latency, budget,
+                                  latency <= budget))
+    return steps, fields
 
 
 # ---------------------------------------------------------------------------

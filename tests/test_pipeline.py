@@ -68,7 +68,8 @@ def test_config_validation():
     with pytest.raises(WhffError):
         pipeline.PipelineConfig(queue_depth=1)
     with pytest.raises(WhffError):
-        pipeline.PipelineConfig(time_source="simulated")
+        pipeline.PipelineConfig(time_source="wallclock")
+    pipeline.PipelineConfig(time_source="simulated")
     with pytest.raises(WhffError):
         pipeline.PipelineConfig(evaluation="approximate")
     cfg = pipeline.PipelineConfig(use_compression=True)

@@ -181,6 +181,11 @@ def scan_small():
         out[f"{tag}_light"] = np.array([s.phase == "light" for s in tr])
         out[f"{tag}_slit"] = np.array([s.slit for s in tr])
         out[f"{tag}_bytes_in"] = np.array([s.bytes_in for s in tr])
+        # the simulated clock's times (pipeline.py:208-289)
+        out[f"{tag}_times"] = np.array([[s.t_transfer, s.t_decode, s.t_compute, s.stage1_start,
+                                         s.stage1_end, s.stage2_start, s.stage2_end] for s in tr])
+        out[f"{tag}_fields"] = np.array([[f.start, f.end, f.latency_s, f.budget_s,
+                                          float(f.deadline_met)] for f in res.trace.fields])
     np.savez_compressed(os.path.join(OUT, "scan_small.npz"), **out)
     print("scan steps", len(tr))
 
