@@ -179,3 +179,41 @@ class DeviceHeatLoad:
         except KeyError:
             raise WhffError(f"no light footprint for field {field_id} slit {slit_id}") from None
         return source_term_device(fp, self.dark, self.dose_scale, out)
+
+
+def source_term(load, field_id, phase, slit_id=None):
+    """thermal.py:81-88 on the device: u_k for one schedule step (binary32
+    fp32(dose) * footprint + dark, or the dark load); returns numpy."""
+    if phase not in ("light", "dark"):
+        raise WhffError(f"step phase must be light or dark, got {phase!r}")
+    fps = {} if phase == "dark" else {(field_id, slit_id): load.light_load(field_id, slit_id)}
+    dev = DeviceHeatLoad(load.dark_load, fps, load.dose_scale)
+    return dev.source(field_id, phase, slit_id).cpu().numpy()
+
+
+def run_field_thermal(model, field_schedule, load, state, A=None, P=None, B=None):
+    """thermal.py:120-140 on the device: advance `state` (a device
+    ThermalState) across one field, yielding (k, phase, slit, S_next) with
+    S_next a CUDA tensor for light steps and None for dark ones.  A, P, B
+    (DeviceCSR / tensor) may be passed to reuse uploaded operators."""
+    torch = _lib.require_cuda()
+    A = A if A is not None else DeviceCSR(model.A_f64())
+    P = P if P is not None else DeviceCSR(model.P_f64())
+    B = B if B is not None else torch.from_numpy(np.ascontiguousarray(model.B, np.float32)).cuda()
+    n_slits = model.n_slits(field_schedule.field_id)
+    keys = {(field_schedule.field_id, field_schedule.slit_for_light_step(i, n_slits))
+            for i in range(field_schedule.t_l)}
+    dev = DeviceHeatLoad(load.dark_load, {k: load.light_load(*k) for k in keys}, load.dose_scale)
+    u = torch.empty_like(state.temperatures)
+    for i in range(field_schedule.t_l + field_schedule.t_d):
+        if i < field_schedule.t_l:
+            phase, slit = "light", field_schedule.slit_for_light_step(i, n_slits)
+        else:
+            phase, slit = "dark", None
+        dev.source(field_schedule.field_id, phase, slit, out=u)
+        t_next = csr_matvec(A, state.temperatures, B, u)
+        s_next = csr_matvec(P, t_next)
+        state.k += 1
+        state.temperatures = t_next
+        state.interpolated = s_next
+        yield state.k, phase, slit, (s_next if phase == "light" else None)
