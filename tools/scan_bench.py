@@ -3,7 +3,7 @@ x 378 x 256,000 per axis (compressed on the GPU), fast schedule (34 light + 36
 dark ms, 50 ms budget), paced at 1 ms per step on the device clock and
 unpaced; slits resident in HBM, and streamed from pinned host memory through
 a 4-slot ring (the reference's stage 1).  One JSON line.
-Usage: python tools/scan_bench.py [n_fields] [mode] [evaluation]"""
+Usage: python tools/scan_bench.py [n_fields] [mode] [evaluation] [ring slots]"""
 import json
 import os
 import statistics
@@ -16,6 +16,7 @@ from paper_1902_08018_b200 import codec, model, pipeline, thermal  # noqa: E402
 n_fields = int(sys.argv[1]) if len(sys.argv) > 1 else 2
 mode_s = sys.argv[2] if len(sys.argv) > 2 else "rate:8"
 ev = sys.argv[3] if len(sys.argv) > 3 else "coefficient"
+depth = int(sys.argv[4]) if len(sys.argv) > 4 else 4      # streaming ring slots
 kind, p = mode_s.split(":")
 mode = {"rate": codec.FixedRate, "precision": codec.FixedPrecision,
         "accuracy": codec.FixedAccuracy}[kind](int(p) if kind != "accuracy" else float(p))
@@ -32,7 +33,8 @@ variants = [("paced_1ms", 1e-3, False), ("unpaced", None, False),
             ("streaming_paced_1ms", 1e-3, True), ("streaming_unpaced", None, True)]
 for tag, period, streaming in variants:
     cfg = pipeline.PipelineConfig(use_compression=True, codec_mode=mode, evaluation=ev,
-                                  step_period_s=period, streaming=streaming, queue_depth=4)
+                                  step_period_s=period, streaming=streaming,
+                                  queue_depth=depth if streaming else 2)
     t1 = time.time()
     res = pipeline.run_scan(m, sched, hl, cfg)
     wall = time.time() - t1
