@@ -200,8 +200,13 @@ WHFF_HD void unroll16_live(uint32_t live, F&& f) {
     }
   }
 }
-WHFF_HD uint32_t top_mask(int nbits) {  // top nbits set, nbits in [0, 32]
+WHFF_HD uint32_t top_mask(int nbits) {  // top nbits set (nbits clamped to [0, 32])
+#if defined(__CUDA_ARCH__)
+  // ~(0xFFFFFFFF >> n) with the funnel shift's clamp at 32: 2 instructions
+  return ~__funnelshift_rc(0xFFFFFFFFu, 0u, (uint32_t)max(nbits, 0));
+#else
   return nbits <= 0 ? 0u : (nbits >= 32 ? 0xFFFFFFFFu : ~(0xFFFFFFFFu >> nbits));
+#endif
 }
 
 struct BitWin {
