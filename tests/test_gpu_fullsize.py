@@ -54,12 +54,16 @@ def test_full_width_slit(orc, kind, param):
     v = torch.rand(S_COLS, device="cuda")
     y_ref = gemv_device(words, v, "mixed", "sequential")
     bound = (S_COLS + 1) * EPS32 * (words.abs().double() @ v.abs().double())
+    exact64 = words.double() @ v.double()                 # binary64 ground truth (mpgemv.py:64-69)
     for ev in ("exact", "coefficient"):
         y = sf.gemv(v, evaluation=ev)
         err = (y.double() - y_ref.double()).abs()
         assert bool((err <= bound).all()), ev
         if ev == "exact":
             assert float((y.view(torch.int32) == y_ref.view(torch.int32)).double().mean()) >= 0.97
+        # acceptance-3 (tests/test_acceptance.py:73): median relative error <= 1e-7
+        rel = ((y.double() - exact64).abs() / exact64.abs()).median()
+        assert float(rel) <= 1e-7, (ev, float(rel))
 
 
 def test_field_plan_matches_per_slit_launches():
