@@ -546,7 +546,8 @@ def b200_main(args, world, rank, local):
         "n_gpus": world, "steps": args.steps, "warmup": args.warmup,
         "ms_per_step": round(total_ms / args.steps, 4), "higher_is_better": True,
         "scaling": "strong", "vs_baseline": None,
-        "dtype": "f32 products, f64 accumulate" if args.policy == "mixed" else args.policy,
+        "dtype": (("f32 coefficient-domain products, f64 accumulate" if args.evaluation == "coefficient"
+                   else "f32 products, f64 accumulate") if args.policy == "mixed" else args.policy),
         "data": "synthetic (reference smooth-C formula model.py:252-268, seed 7); "
                 f"{info['distinct_per_axis']} distinct slits/axis",
         "config": {"workload": "paper-scale WHFF step (configs[2]): thermal T=608^2 nnz7 + "
