@@ -281,12 +281,25 @@ struct GemvJob {
   uint64_t br0;        // first block-row of the job
 };
 
+// Per-virtual-warp partial sums of one block-row (see k_decode_gemv).
+struct VwRec {
+  double d[4];
+  double r[4];
+  float f[4];
+  float rf[4];
+  float probe;
+  float pad;
+};
+
 struct JobTable {
   const GemvJob* jobs;       // device table (plans) or nullptr
-  const uint64_t* prefix;    // first global warp of each job
+  const uint64_t* prefix;    // first block-row of each job
+  const uint32_t* row_job;   // job of each block-row
   int n;
-  uint64_t total_warps;
+  uint64_t total_warps;      // block-rows
   GemvJob single;            // used when jobs == nullptr
+  VwRec* recs;               // [block-row][kVW] partials
+  unsigned* tickets;         // [block-row] warp arrival counters (zero between launches)
 };
 
 // G = real-valued inverse lift (codec.py:128-134 with >>1 -> /2, <<1 -> *2);
@@ -408,6 +421,15 @@ __device__ __noinline__ void coef_fallback(const uint32_t* words, uint64_t start
 }
 
 constexpr int kGemvWarps = 8;
+// A block-row's 32-block groups are summed in kVW "virtual warps": virtual
+// warp w takes groups w, w + kVW, w + 2 kVW, ... (one partial per lane, then
+// a fixed butterfly).  Each row runs on kSplit CTAs of 8 warps (one virtual
+// warp per warp), so launches with few block-rows (a light step: 3 slits =
+// 285 rows) still fill the GPU; the last of the row's warps to finish adds
+// the kVW partials with another fixed butterfly.  The order is fixed, so a
+// row's result does not depend on the launch that computes it.
+constexpr int kVW = 32;
+constexpr int kSplit = kVW / kGemvWarps;   // CTAs per block-row
 
 // Software-pipelined segment location for indexed / implicit variable-rate
 // streams (see k_decode_gemv).  Holds, for the next group, its start bit,
@@ -460,17 +482,18 @@ struct SegPrefetch {
       a0 = ldg(p); a1 = ldg(p + 1); a2 = ldg(p + 2); a3 = ldg(p + 3);
     }
   }
+  // a warp's groups are g0, g0 + kVW, g0 + 2 kVW, ... (see kVW)
   __device__ __forceinline__ void prologue(const StreamView& s, uint64_t brow, uint64_t row_block0,
                                            uint64_t bc, uint64_t g0, int lane) {
     load_index(s, brow, row_block0, bc, g0, lane);
     locate(s, row_block0, bc, g0, lane);
-    load_index(s, brow, row_block0, bc, g0 + kGemvWarps, lane);
+    load_index(s, brow, row_block0, bc, g0 + kVW, lane);
   }
-  // called at group g with gn = g + 8: locate gn, fetch the index of gn + 8
+  // called at group g with gn = g + kVW: locate gn, fetch the index of gn + kVW
   __device__ __forceinline__ void advance(const StreamView& s, uint64_t brow, uint64_t row_block0,
                                           uint64_t bc, uint64_t gn, int lane) {
     locate(s, row_block0, bc, gn, lane);
-    load_index(s, brow, row_block0, bc, gn + kGemvWarps, lane);
+    load_index(s, brow, row_block0, bc, gn + kVW, lane);
   }
 };
 
@@ -485,33 +508,40 @@ template <> struct VarTraits<2> { static constexpr bool kRefill = true, kRaw = f
 // 3: indexed with raw flag (fixed accuracy)
 template <> struct VarTraits<3> { static constexpr bool kRefill = true, kRaw = true, kIndexed = true; };
 
-// launch bounds: plain 256 lets ptxas settle at 64 registers (4 CTAs/SM),
-// measured best for the fused kernel; -DWHFF_GEMV_MINB=n overrides for sweeps
+// launch bounds: fixed-rate variants are held at 64 registers (4 CTAs/SM),
+// measured best for the fused kernel; the indexed ones settle at 74-80 (3
+// CTAs/SM) on their own; -DWHFF_GEMV_MINB=n overrides for sweeps
 #ifdef WHFF_GEMV_MINB
 #define WHFF_GEMV_LB __launch_bounds__(256, WHFF_GEMV_MINB)
 #else
-#define WHFF_GEMV_LB __launch_bounds__(256)
+#define WHFF_GEMV_LB __launch_bounds__(256, VAR <= 1 ? 4 : 3)
 #endif
 
 template <int VAR, int EVAL, bool SF, int POL>
 __global__ void WHFF_GEMV_LB k_decode_gemv(JobTable T, unsigned long long* status) {
   using TR = VarTraits<VAR>;
   constexpr int policy = POL;   // compile-time: only the policy's accumulators exist
-  // one CTA per (job, block-row); its 8 warps split the row's 32-block groups
-  const uint64_t gr = blockIdx.x;
+  // kSplit CTAs per (job, block-row); warp w of CTA part q runs the row's
+  // virtual warp 8 q + w (see kVW)
+  const uint64_t gr = blockIdx.x / kSplit;
+  const int part = (int)(blockIdx.x % kSplit);
   if (gr >= T.total_warps) return;
   const int lane = threadIdx.x & 31;
   const int warp = threadIdx.x >> 5;
   uint64_t first_row = 0;
   int jidx = -1;
   if (T.jobs != nullptr) {
-    int lo = 0, hi = T.n - 1;
-    while (lo < hi) {
-      const int mid = (lo + hi + 1) >> 1;
-      if (T.prefix[mid] <= gr) lo = mid; else hi = mid - 1;
+    if (VAR == 0) {           // (the search measured faster here than the table, by codegen)
+      int lo = 0, hi = T.n - 1;
+      while (lo < hi) {
+        const int mid = (lo + hi + 1) >> 1;
+        if (T.prefix[mid] <= gr) lo = mid; else hi = mid - 1;
+      }
+      jidx = lo;
+    } else {
+      jidx = (int)T.row_job[gr];
     }
-    jidx = lo;
-    first_row = T.prefix[lo];
+    first_row = T.prefix[jidx];
   }
   const StreamView s = jidx < 0 ? T.single.s : T.jobs[jidx].s;
   const float* __restrict__ v = jidx < 0 ? T.single.v : T.jobs[jidx].v;
@@ -537,23 +567,28 @@ __global__ void WHFF_GEMV_LB k_decode_gemv(JobTable T, unsigned long long* statu
   for (int i = 0; i < 4; ++i) { RS.d[i] = 0.0; RS.f[i] = 0.0f; }
   RS.probe = 0.0f;
 
+  // this warp's groups: vw, vw + kVW, ... (< gpr)
+  const int vw = part * kGemvWarps + warp;
+
   const uint64_t row_block0 = brow * bc;
   const uint4* __restrict__ seg128 = reinterpret_cast<const uint4*>(s.words);
   uint4 nxt = make_uint4(0, 0, 0, 0);
   // FixedRate(8): the payload covers this block-row's segments completely
   const bool row_full = VAR == 0 && (row_block0 + bc) * 128ull <= s.payload_bits;
   if (VAR == 0) {
-    const uint64_t bcol0 = (uint64_t)warp * 32 + lane;
+    const uint64_t bcol0 = (uint64_t)vw * 32 + lane;
     if (bcol0 < bc) nxt = ldg(seg128 + row_block0 + bcol0);
   }
-  // Variable-length streams: the segment of group g+8 is located (index
+  // Variable-length streams: the segment of the next group is located (index
   // loaded one iteration earlier) and its four payload words are loaded
-  // while group g decodes; the index of g+16 is loaded at the same time.
+  // while group g decodes; the index of the group after is loaded meanwhile.
   SegPrefetch<TR::kIndexed> pf;
-  if (VAR != 0) pf.prologue(s, brow, row_block0, bc, (uint64_t)warp, lane);
+  if (VAR != 0) pf.prologue(s, brow, row_block0, bc, (uint64_t)vw, lane);
 
-  for (uint64_t g = warp; g < s.gpr; g += kGemvWarps) {
-    const uint64_t bcol = g * 32 + lane;
+  // (32-bit group index for FixedRate(8): measured fewer instructions)
+  using GI = typename std::conditional<VAR == 0, uint32_t, uint64_t>::type;
+  for (GI g = vw; g < (GI)s.gpr; g += kVW) {
+    const uint64_t bcol = (uint64_t)g * 32 + lane;
     const bool active = bcol < bc;
     const uint64_t b = row_block0 + bcol;
     BitWin bw;
@@ -571,7 +606,7 @@ __global__ void WHFF_GEMV_LB k_decode_gemv(JobTable T, unsigned long long* statu
     }
     if (VAR == 0) {
       const uint4 q = nxt;
-      const uint64_t bn = bcol + 32 * kGemvWarps;
+      const uint64_t bn = bcol + 32 * kVW;
       if (bn < bc) nxt = ldg(seg128 + row_block0 + bn);   // prefetch this warp's next group
       if (row_full) {                        // every segment of the row is whole: no masks
         fb_len = 128;                        // (lanes past the row end decode zeros, discarded)
@@ -587,7 +622,7 @@ __global__ void WHFF_GEMV_LB k_decode_gemv(JobTable T, unsigned long long* statu
       const uint64_t start = pf.start;
       const int len = pf.len;
       const uint32_t a0 = pf.a0, a1 = pf.a1, a2 = pf.a2, a3 = pf.a3;
-      pf.advance(s, brow, row_block0, bc, g + kGemvWarps, lane);
+      pf.advance(s, brow, row_block0, bc, g + kVW, lane);
       if (active) {
         win_words(bw, s.words, start, len, a0, a1, a2, a3);
       } else {
@@ -648,46 +683,69 @@ __global__ void WHFF_GEMV_LB k_decode_gemv(JobTable T, unsigned long long* statu
 #pragma unroll
   for (int i = 0; i < 4; ++i) { accR[i] = RS.d[i]; accRf[i] = RS.f[i]; }
   if (EVAL == WHFF_EVAL_COEFF) A.probe = __fadd_rn(A.probe, RS.probe);
-  // fixed xor butterfly over the warp, then the 8 warps in order (deterministic)
+  // fixed xor butterfly over the warp (only the policy's accumulators)
+  constexpr bool kF = policy == WHFF_POLICY_SINGLE, kD = !kF, kC = EVAL == WHFF_EVAL_COEFF;
 #pragma unroll
   for (int o = 16; o > 0; o >>= 1) {
 #pragma unroll
     for (int i = 0; i < 4; ++i) {
-      A.d[i] = __dadd_rn(A.d[i], __shfl_xor_sync(0xFFFFFFFFu, A.d[i], o));
-      A.f[i] = __fadd_rn(A.f[i], __shfl_xor_sync(0xFFFFFFFFu, A.f[i], o));
-      if (EVAL == WHFF_EVAL_COEFF) {
-        accR[i] = __dadd_rn(accR[i], __shfl_xor_sync(0xFFFFFFFFu, accR[i], o));
-        accRf[i] = __fadd_rn(accRf[i], __shfl_xor_sync(0xFFFFFFFFu, accRf[i], o));
-      }
+      if (kD) A.d[i] = __dadd_rn(A.d[i], __shfl_xor_sync(0xFFFFFFFFu, A.d[i], o));
+      if (kF) A.f[i] = __fadd_rn(A.f[i], __shfl_xor_sync(0xFFFFFFFFu, A.f[i], o));
+      if (kC && kD) accR[i] = __dadd_rn(accR[i], __shfl_xor_sync(0xFFFFFFFFu, accR[i], o));
+      if (kC && kF) accRf[i] = __fadd_rn(accRf[i], __shfl_xor_sync(0xFFFFFFFFu, accRf[i], o));
     }
-    A.probe = __fadd_rn(A.probe, __shfl_xor_sync(0xFFFFFFFFu, A.probe, o));
+    if (kF) A.probe = __fadd_rn(A.probe, __shfl_xor_sync(0xFFFFFFFFu, A.probe, o));
   }
-  __shared__ double sd[kGemvWarps][4], sR[kGemvWarps][4];
-  __shared__ float sf[kGemvWarps][4], sRf[kGemvWarps][4], sp[kGemvWarps];
+  // publish this virtual warp's partials; the last of the row's kVW warps to
+  // finish adds the kVW partials (fixed xor butterfly) and writes the rows
+  // (row and virtual warp recomputed: nothing extra stays live across the loop)
+  VwRec* grec = T.recs + (uint64_t)(blockIdx.x / kSplit) * kVW;
+  unsigned last = 0;
   if (lane == 0) {
+    VwRec R;
 #pragma unroll
     for (int i = 0; i < 4; ++i) {
-      sd[warp][i] = A.d[i];
-      sf[warp][i] = A.f[i];
-      sR[warp][i] = accR[i];
-      sRf[warp][i] = accRf[i];
+      R.d[i] = A.d[i];
+      R.f[i] = A.f[i];
+      R.r[i] = EVAL == WHFF_EVAL_COEFF ? accR[i] : 0.0;
+      R.rf[i] = EVAL == WHFF_EVAL_COEFF ? accRf[i] : 0.0f;
     }
-    sp[warp] = A.probe;
+    R.probe = A.probe;
+    R.pad = 0.0f;
+    grec[(blockIdx.x % kSplit) * kGemvWarps + (threadIdx.x >> 5)] = R;
+    __threadfence();
+    last = atomicInc(T.tickets + blockIdx.x / kSplit, kVW - 1u) == kVW - 1u;
   }
-  __syncthreads();
-  if (threadIdx.x < 4) {
-    const int i = threadIdx.x;
-    double td[4] = {0.0, 0.0, 0.0, 0.0}, tR = 0.0;
-    float tf[4] = {0.0f, 0.0f, 0.0f, 0.0f}, tRf = 0.0f, probe = 0.0f;
-    for (int w = 0; w < kGemvWarps; ++w) {
+  if (!__shfl_sync(0xFFFFFFFFu, last, 0)) return;
+  __threadfence();
+  VwRec P;
+  {
+    const unsigned long long* src = reinterpret_cast<const unsigned long long*>(grec + lane);
+    unsigned long long* dst = reinterpret_cast<unsigned long long*>(&P);
 #pragma unroll
-      for (int a = 0; a < 4; ++a) {
-        td[a] = __dadd_rn(td[a], sd[w][a]);
-        tf[a] = __fadd_rn(tf[a], sf[w][a]);
-      }
-      tR = __dadd_rn(tR, sR[w][i]);
-      tRf = __fadd_rn(tRf, sRf[w][i]);
-      probe = __fadd_rn(probe, sp[w]);
+    for (int k = 0; k < (int)(sizeof(VwRec) / 8); ++k) dst[k] = __ldcg(src + k);
+  }
+#pragma unroll
+  for (int o = 16; o > 0; o >>= 1) {
+#pragma unroll
+    for (int a = 0; a < 4; ++a) {
+      if (kD) P.d[a] = __dadd_rn(P.d[a], __shfl_xor_sync(0xFFFFFFFFu, P.d[a], o));
+      if (kF) P.f[a] = __fadd_rn(P.f[a], __shfl_xor_sync(0xFFFFFFFFu, P.f[a], o));
+      if (kC && kD) P.r[a] = __dadd_rn(P.r[a], __shfl_xor_sync(0xFFFFFFFFu, P.r[a], o));
+      if (kC && kF) P.rf[a] = __fadd_rn(P.rf[a], __shfl_xor_sync(0xFFFFFFFFu, P.rf[a], o));
+    }
+    if (kF) P.probe = __fadd_rn(P.probe, __shfl_xor_sync(0xFFFFFFFFu, P.probe, o));
+  }
+  if (lane < 4) {
+    const int i = lane;
+    double td[4], tR = 0.0;
+    float tf[4], tRf = 0.0f;
+    const float probe = P.probe;
+#pragma unroll
+    for (int a = 0; a < 4; ++a) {
+      td[a] = P.d[a];
+      tf[a] = P.f[a];
+      if (a == i) { tR = P.r[a]; tRf = P.rf[a]; }
     }
     const uint64_t r = brow * 4 + i;
     if (r >= row_begin && r < row_end && r < s.rows) {
@@ -1637,7 +1695,7 @@ template <int EVAL, bool SF, int POL>
 static void launch_gemv_pol(int var, const JobTable& T, unsigned long long* status,
                             cudaStream_t cs) {
   const unsigned threads = 32 * kGemvWarps;
-  const unsigned blocks = (unsigned)T.total_warps;   // one CTA per block-row
+  const unsigned blocks = (unsigned)(T.total_warps * kSplit);   // kSplit CTAs per block-row
   switch (var) {
     case 0: k_decode_gemv<0, EVAL, SF, POL><<<blocks, threads, 0, cs>>>(T, status); break;
     case 1: k_decode_gemv<1, EVAL, SF, POL><<<blocks, threads, 0, cs>>>(T, status); break;
@@ -1669,9 +1727,19 @@ static whff_status_t launch_gemv(int var, int eval, bool sf, const JobTable& T, 
   return launch_gemv_var<WHFF_EVAL_EXACT, false>(var, T, policy, status, cs);
 }
 
+// single-call workspace: [G^T v per block-column (coefficient evaluation)]
+// [per-row virtual-warp partials][per-row arrival counters]
+static uint64_t align256(uint64_t x) { return (x + 255) & ~255ull; }
+static uint64_t ws_u_bytes(const whff_dstream* s, int eval) {
+  return eval == WHFF_EVAL_COEFF ? align256(s->bc * sizeof(float4)) : 0;
+}
+static uint64_t ws_rec_bytes(const whff_dstream* s) {
+  return align256(std::max<uint64_t>(s->br, 1) * kVW * sizeof(VwRec));
+}
+
 extern "C" whff_status_t whff_decode_gemv_workspace_size(whff_dstream_t s, int eval, size_t* bytes) {
   if (!s || !bytes) return fail(WHFF_ERR_ARGUMENT, "null argument");
-  *bytes = eval == WHFF_EVAL_COEFF ? s->bc * sizeof(float4) : 0;
+  *bytes = ws_u_bytes(s, eval) + ws_rec_bytes(s) + std::max<uint64_t>(s->br, 1) * sizeof(unsigned);
   return WHFF_OK;
 }
 
@@ -1696,6 +1764,7 @@ extern "C" whff_status_t whff_decode_gemv(whff_dstream_t s, const float* v, floa
   JobTable T;
   T.jobs = nullptr;
   T.prefix = nullptr;
+  T.row_job = nullptr;
   T.n = 1;
   T.single.s = s->view();
   T.single.v = v;
@@ -1705,9 +1774,16 @@ extern "C" whff_status_t whff_decode_gemv(whff_dstream_t s, const float* v, floa
   T.single.row_end = row_end;
   T.single.br0 = row_begin / 4;
   T.total_warps = (row_end + 3) / 4 - row_begin / 4;
+  size_t need = 0;
+  whff_decode_gemv_workspace_size(s, eval, &need);
+  if (!ws || ws_bytes < need) return fail(WHFF_ERR_ARGUMENT, "workspace too small");
+  if ((reinterpret_cast<uintptr_t>(ws) & 15u) != 0) return fail(WHFF_ERR_ARGUMENT, "workspace alignment");
+  uint8_t* wsb = reinterpret_cast<uint8_t*>(ws);
+  T.recs = reinterpret_cast<VwRec*>(wsb + ws_u_bytes(s, eval));
+  T.tickets = reinterpret_cast<unsigned*>(wsb + ws_u_bytes(s, eval) + ws_rec_bytes(s));
+  cudaError_t me = cudaMemsetAsync(T.tickets, 0, T.total_warps * sizeof(unsigned), cs);
+  if (me != cudaSuccess) return cuda_fail(me, "workspace clear");
   if (eval == WHFF_EVAL_COEFF) {
-    if (!ws || ws_bytes < s->bc * sizeof(float4)) return fail(WHFF_ERR_ARGUMENT, "workspace too small");
-    if ((reinterpret_cast<uintptr_t>(ws) & 15u) != 0) return fail(WHFF_ERR_ARGUMENT, "workspace alignment");
     k_coeff_prep<<<grid_for(s->bc, 256), 256, 0, cs>>>(v, s->cols, s->bc, reinterpret_cast<float4*>(ws));
     WCK_LAUNCH("coeff_prep");
     T.single.U = reinterpret_cast<const float4*>(ws);
@@ -1723,8 +1799,11 @@ struct whff_gemv_plan {
   bool sf = false;
   GemvJob* d_jobs = nullptr;
   uint64_t* d_prefix = nullptr;
+  uint32_t* d_row_job = nullptr;
   uint64_t total_warps = 0;
   float4* d_U = nullptr;
+  VwRec* d_recs = nullptr;       // [block-row][kVW] partials
+  unsigned* d_tickets = nullptr;  // [block-row] arrival counters (reset by the kernel)
   // distinct vectors for the coefficient prologue
   std::vector<const float*> prep_v;
   std::vector<uint64_t> prep_cols, prep_bc, prep_off;
@@ -1804,10 +1883,26 @@ whff_status_t whff_gemv_plan_create(int n, const whff_dstream_t* streams, const 
   if (e == cudaSuccess) e = cudaMalloc(&P->d_prefix, n * sizeof(uint64_t));
   if (e == cudaSuccess) e = cudaMemcpy(P->d_jobs, jobs.data(), n * sizeof(GemvJob), cudaMemcpyHostToDevice);
   if (e == cudaSuccess) e = cudaMemcpy(P->d_prefix, prefix.data(), n * 8, cudaMemcpyHostToDevice);
+  {
+    std::vector<uint32_t> row_job(std::max<uint64_t>(warps, 1), 0u);
+    for (int i = 0; i < n; ++i) {
+      const uint64_t end = i + 1 < n ? prefix[i + 1] : warps;
+      for (uint64_t r = prefix[i]; r < end; ++r) row_job[r] = (uint32_t)i;
+    }
+    if (e == cudaSuccess) e = cudaMalloc(&P->d_row_job, row_job.size() * sizeof(uint32_t));
+    if (e == cudaSuccess)
+      e = cudaMemcpy(P->d_row_job, row_job.data(), row_job.size() * sizeof(uint32_t), cudaMemcpyHostToDevice);
+  }
+  if (e == cudaSuccess) e = cudaMalloc(&P->d_recs, std::max<uint64_t>(warps, 1) * kVW * sizeof(VwRec));
+  if (e == cudaSuccess) e = cudaMalloc(&P->d_tickets, std::max<uint64_t>(warps, 1) * sizeof(unsigned));
+  if (e == cudaSuccess) e = cudaMemset(P->d_tickets, 0, std::max<uint64_t>(warps, 1) * sizeof(unsigned));
   if (e != cudaSuccess) {
     cudaFree(P->d_U);
     cudaFree(P->d_jobs);
     cudaFree(P->d_prefix);
+    cudaFree(P->d_row_job);
+    cudaFree(P->d_recs);
+    cudaFree(P->d_tickets);
     delete P;
     return cuda_fail(e, "plan create");
   }
@@ -1828,9 +1923,12 @@ whff_status_t whff_gemv_plan_launch(whff_gemv_plan_t P, uint64_t* status, whff_s
   JobTable T;
   T.jobs = P->d_jobs;
   T.prefix = P->d_prefix;
+  T.row_job = P->d_row_job;
   T.n = P->n;
   T.total_warps = P->total_warps;
   memset(&T.single, 0, sizeof(T.single));
+  T.recs = P->d_recs;
+  T.tickets = P->d_tickets;
   return launch_gemv(P->var, P->eval, P->sf, T, P->policy, reinterpret_cast<unsigned long long*>(status), cs);
 }
 
@@ -1848,6 +1946,9 @@ whff_status_t whff_gemv_plan_destroy(whff_gemv_plan_t P) {
   cudaFree(P->d_U);
   cudaFree(P->d_jobs);
   cudaFree(P->d_prefix);
+  cudaFree(P->d_row_job);
+  cudaFree(P->d_recs);
+  cudaFree(P->d_tickets);
   delete P;
   return WHFF_OK;
 }
