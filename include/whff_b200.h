@@ -217,7 +217,11 @@ whff_status_t whff_decode(whff_dstream_t s, float* out_dev, uint64_t ld_out,
 
 /* y[r - row_begin] = sum_j C[r, j] * v[j] for r in [row_begin, row_end),
  * C the decoded stream.  v_dev has `cols` floats, y_dev row_end-row_begin.
- * workspace: whff_decode_gemv_workspace_size bytes (device), or NULL if 0. */
+ * workspace: whff_decode_gemv_workspace_size bytes of device memory, 16-byte
+ * aligned, any contents (the per-row partial sums and arrival counters; for
+ * the coefficient evaluation also G^T v).  A row's result does not depend on
+ * the row range or on batching (plans give the same bits).  Calls sharing a
+ * workspace must be ordered (one stream).                                  */
 whff_status_t whff_decode_gemv_workspace_size(whff_dstream_t s, int eval, size_t* bytes);
 whff_status_t whff_decode_gemv(whff_dstream_t s, const float* v_dev, float* y_dev,
                                int policy, int eval, uint64_t row_begin, uint64_t row_end,
@@ -225,9 +229,10 @@ whff_status_t whff_decode_gemv(whff_dstream_t s, const float* v_dev, float* y_de
                                uint64_t* status_dev, whff_stream_t stream);
 
 /* Batched plan: n jobs (stream, vector, output, row range) executed by one
- * persistent launch per call -- the per-light-step deformation products of
+ * launch per call -- the per-light-step deformation products of
  * pipeline.py:199-205 over many slit streams.  Creation builds the device
- * job table (synchronous); launch is capture-safe (CUDA graphs).  All
+ * job table and the plan's workspace (synchronous); launch is capture-safe
+ * (CUDA graphs); launches of one plan must be ordered (one stream).  All
  * streams of a plan must share mode, index kind and raw flag.             */
 whff_status_t whff_gemv_plan_create(int n_jobs, const whff_dstream_t* streams,
                                     const float* const* v_dev, float* const* y_dev,
