@@ -550,8 +550,10 @@ def b200_main(args, world, rank, local):
                    else "f32 products, f64 accumulate") if args.policy == "mixed" else args.policy),
         "data": "synthetic (reference smooth-C formula model.py:252-268, seed 7); "
                 f"{info['distinct_per_axis']} distinct slits/axis",
-        "config": {"workload": "paper-scale WHFF step (configs[2]): thermal T=608^2 nnz7 + "
-                               f"3 axes x {args.slits} slits x {args.rows}x{args.S}",
+        "config": {"workload": (("paper-scale WHFF step (configs[2])" if (args.S, args.grid) == (256000, 608)
+                                 else "4x paper mesh step (configs[4] workload)" if args.S == 1024000
+                                 else "WHFF step") + f": thermal T={args.grid}^2 nnz7 + "
+                                f"3 axes x {args.slits} slits x {args.rows}x{args.S}"),
                    "mode": args.mode, "evaluation": args.evaluation, "policy": args.policy,
                    "layout": args.layout,
                    "parallelism": f"row-shard{world}" if world > 1 else "single",
