@@ -560,9 +560,12 @@ __global__ void WHFF_GEMV_LB k_decode_gemv(JobTable T, unsigned long long* statu
 #pragma unroll
   for (int i = 0; i < 4; ++i) { A.d[i] = 0.0; A.f[i] = 0.0f; }
   A.probe = 0.0f;
-  // coefficient domain: spatial part of the rare raw / extreme-scale blocks
-  // (its address goes to the out-of-line fallback, so it lives in local memory)
-  Acc RS;
+  // coefficient domain: spatial part of the rare raw / extreme-scale blocks.
+  // Its address goes to the out-of-line fallback, so it lives in memory: in
+  // shared memory, since a local-memory frame zeroed by every thread of every
+  // CTA was written back to HBM (0.95 GB per config-3 step).
+  __shared__ Acc s_rs[32 * kGemvWarps];
+  Acc& RS = s_rs[threadIdx.x];
 #pragma unroll
   for (int i = 0; i < 4; ++i) { RS.d[i] = 0.0; RS.f[i] = 0.0f; }
   RS.probe = 0.0f;
