@@ -716,11 +716,15 @@ __global__ void WHFF_GEMV_LB k_decode_gemv(JobTable T, unsigned long long* statu
     R.probe = A.probe;
     R.pad = 0.0f;
     grec[(blockIdx.x % kSplit) * kGemvWarps + (threadIdx.x >> 5)] = R;
-    __threadfence();
-    last = atomicInc(T.tickets + blockIdx.x / kSplit, kVW - 1u) == kVW - 1u;
+    // release: the record is visible before the count (no full fence: a
+    // gpu-scope __threadfence per warp also invalidated the SM's L1)
+    unsigned old;
+    asm volatile("atom.release.gpu.global.inc.u32 %0, [%1], %2;"
+                 : "=r"(old) : "l"(T.tickets + blockIdx.x / kSplit), "r"(kVW - 1u) : "memory");
+    last = old == kVW - 1u;
   }
   if (!__shfl_sync(0xFFFFFFFFu, last, 0)) return;
-  __threadfence();
+  asm volatile("fence.acq_rel.gpu;" ::: "memory");   // the other warps' records (read via L2)
   VwRec P;
   {
     const unsigned long long* src = reinterpret_cast<const unsigned long long*>(grec + lane);
