@@ -1,5 +1,6 @@
 """Launch-independent row sums: every block-row runs on 4 CTAs of 8 warps
-whose 32 virtual-warp partials the last CTA to finish adds in a fixed order.
+whose 32 virtual-warp partials the last warp to finish adds with a fixed
+butterfly.
 
 A row's result must therefore be bit-identical whichever launch computes it:
 a single call, a single call over a row sub-range, a one-job plan, or a plan
@@ -102,3 +103,32 @@ def test_plan_relaunch_and_single_call_workspace(rng):
         st = _lib.status_word()
         _lib.call("whff_decode_gemv", ds.handle, _lib.ptr(v), _lib.ptr(y), _lib.POLICY["mixed"],
                   _lib.EVAL["exact"], 0, 64, _lib.ptr(ws_small), 16, _lib.ptr(st), _lib.cur_stream())
+
+
+def test_concurrent_plans_on_two_streams(rng):
+    """Distinct plans (own partials and counters) over one resident stream,
+    launched concurrently on two CUDA streams: each gives the single-call bits."""
+    import torch
+    from paper_1902_08018_b200 import _lib, codec
+    from paper_1902_08018_b200.executor import GemvPlan
+    C = smooth_matrix(96, 30011, seed=8)
+    ds = codec.DeviceStream.from_host(codec.compress(C, codec.FixedRate(8))).relayout("skeleton-first")
+    v1 = torch.from_numpy(rng.random(C.shape[1]).astype(np.float32)).cuda()
+    v2 = torch.from_numpy(rng.random(C.shape[1]).astype(np.float32)).cuda()
+    ref1 = ds.gemv(v1, evaluation="coefficient").cpu().numpy()
+    ref2 = ds.gemv(v2, evaluation="coefficient").cpu().numpy()
+    o1, o2 = torch.zeros(96, device="cuda"), torch.zeros(96, device="cuda")
+    p1 = GemvPlan([(ds, v1, o1, 0, 96)], evaluation="coefficient")
+    p2 = GemvPlan([(ds, v2, o2, 0, 96)], evaluation="coefficient")
+    s1, s2 = torch.cuda.Stream(), torch.cuda.Stream()
+    st1, st2 = _lib.status_word(), _lib.status_word()
+    torch.cuda.synchronize()
+    for _ in range(20):
+        with torch.cuda.stream(s1):
+            p1.launch(st1)
+        with torch.cuda.stream(s2):
+            p2.launch(st2)
+    torch.cuda.synchronize()
+    assert same(o1.cpu().numpy(), ref1) and same(o2.cpu().numpy(), ref2)
+    p1.close()
+    p2.close()
