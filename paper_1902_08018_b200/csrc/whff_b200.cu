@@ -875,9 +875,13 @@ __global__ void k_tree_store(const T* in, uint64_t rows, float* y) {
   if (i < rows) y[i] = (float)in[i];
 }
 
-// B200 blocked order: warp per (row, segment of seg_cols columns), float4
-// loads, per-lane accumulation, xor butterfly; partials summed in segment
-// order by k_blocked_finish.  Deterministic for a given shape.
+// B200 blocked order: warp per (row, segment of seg_cols columns).  Each lane
+// issues kBlkU 16-byte loads of the row (streaming, evict-first) and of the
+// vector before using any of them, so a warp keeps kBlkU x 512 B in flight;
+// two accumulators per lane (even / odd float4 of the batch) break the add
+// chain.  Partials: xor butterfly, then k_blocked_finish adds the segments in
+// order.  Deterministic for a given shape.
+constexpr int kBlkU = 8;
 template <int POL>
 __global__ void __launch_bounds__(256) k_gemv_blocked(const float* A, uint64_t lda, uint64_t rows,
                                                       uint64_t cols, const float* v, uint64_t nseg,
@@ -889,30 +893,47 @@ __global__ void __launch_bounds__(256) k_gemv_blocked(const float* A, uint64_t l
   const float* row = A + i * lda;
   const uint64_t c0 = sg * seg_cols;
   const uint64_t c1 = min(cols, c0 + seg_cols);
-  double accd = 0.0;
-  float accf = 0.0f;
-  auto add = [&](float a, float b) {
-    if (POL == WHFF_POLICY_SINGLE) accf = __fadd_rn(accf, __fmul_rn(a, b));
-    else if (POL == WHFF_POLICY_MIXED) accd = __dadd_rn(accd, (double)__fmul_rn(a, b));
-    else accd = __dadd_rn(accd, __dmul_rn((double)a, (double)b));
+  double accd[2] = {0.0, 0.0};
+  float accf[2] = {0.0f, 0.0f};
+  auto add = [&](int k, float a, float b) {
+    if (POL == WHFF_POLICY_SINGLE) accf[k] = __fadd_rn(accf[k], __fmul_rn(a, b));
+    else if (POL == WHFF_POLICY_MIXED) accd[k] = __dadd_rn(accd[k], (double)__fmul_rn(a, b));
+    else accd[k] = __dadd_rn(accd[k], __dmul_rn((double)a, (double)b));
   };
+  uint64_t j0 = c0;
   if (vec4) {
     const float4* r4 = reinterpret_cast<const float4*>(row);
     const float4* v4 = reinterpret_cast<const float4*>(v);
-    for (uint64_t q = c0 / 4 + lane; q < c1 / 4; q += 32) {
-      const float4 a = ldg(r4 + q), b = ldg(v4 + q);
-      add(a.x, b.x); add(a.y, b.y); add(a.z, b.z); add(a.w, b.w);
+    const uint64_t q1 = c1 / 4;
+    uint64_t q = c0 / 4;                       // c0 is a multiple of 512 (seg_cols)
+    for (; q + 32 * kBlkU <= q1; q += 32 * kBlkU) {
+      float4 a[kBlkU], b[kBlkU];
+#pragma unroll
+      for (int u = 0; u < kBlkU; ++u) {
+        a[u] = __ldcs(r4 + q + 32 * u + lane);
+        b[u] = ldg(v4 + q + 32 * u + lane);
+      }
+#pragma unroll
+      for (int u = 0; u < kBlkU; ++u) {
+        add(u & 1, a[u].x, b[u].x); add(u & 1, a[u].y, b[u].y);
+        add(u & 1, a[u].z, b[u].z); add(u & 1, a[u].w, b[u].w);
+      }
     }
-    for (uint64_t j = (c1 / 4) * 4 + lane; j < c1; j += 32) add(row[j], ldg(v + j));
-  } else {
-    for (uint64_t j = c0 + lane; j < c1; j += 32) add(row[j], ldg(v + j));
+    for (uint64_t r = q + lane; r < q1; r += 32) {
+      const float4 a = __ldcs(r4 + r), b = ldg(v4 + r);
+      add(0, a.x, b.x); add(0, a.y, b.y); add(0, a.z, b.z); add(0, a.w, b.w);
+    }
+    j0 = q1 * 4;
   }
+  for (uint64_t j = j0 + lane; j < c1; j += 32) add(0, row[j], ldg(v + j));
+  double ad = __dadd_rn(accd[0], accd[1]);
+  float af = __fadd_rn(accf[0], accf[1]);
 #pragma unroll
   for (int o = 16; o > 0; o >>= 1) {
-    accd = __dadd_rn(accd, __shfl_xor_sync(0xFFFFFFFFu, accd, o));
-    accf = __fadd_rn(accf, __shfl_xor_sync(0xFFFFFFFFu, accf, o));
+    ad = __dadd_rn(ad, __shfl_xor_sync(0xFFFFFFFFu, ad, o));
+    af = __fadd_rn(af, __shfl_xor_sync(0xFFFFFFFFu, af, o));
   }
-  if (lane == 0) part[gw] = POL == WHFF_POLICY_SINGLE ? (double)accf : accd;
+  if (lane == 0) part[gw] = POL == WHFF_POLICY_SINGLE ? (double)af : ad;
 }
 
 template <int POL>
@@ -1965,12 +1986,14 @@ whff_status_t whff_gemv_plan_destroy(whff_gemv_plan_t P) {
 // ---- dense GEMV -----------------------------------------------------------
 
 static void blocked_split(uint64_t rows, uint64_t cols, uint64_t& nseg, uint64_t& seg_cols) {
-  // enough warps to fill 148 SMs x 16 warps, segments a multiple of 128 cols
-  const uint64_t target = 148ull * 16;
+  // enough warps for 148 SMs x 64 warps; segments a multiple of one batch of
+  // kBlkU float4 per lane (512 columns)
+  constexpr uint64_t kSeg = 128 * kBlkU;
+  const uint64_t target = 148ull * 64;
   nseg = rows >= target ? 1 : (target + rows - 1) / rows;
-  const uint64_t max_seg = std::max<uint64_t>(1, (cols + 127) / 128);
+  const uint64_t max_seg = std::max<uint64_t>(1, (cols + kSeg - 1) / kSeg);
   nseg = std::min(nseg, max_seg);
-  seg_cols = ((cols + nseg - 1) / nseg + 127) / 128 * 128;
+  seg_cols = ((cols + nseg - 1) / nseg + kSeg - 1) / kSeg * kSeg;
   nseg = (cols + seg_cols - 1) / seg_cols;
   if (nseg == 0) nseg = 1;
 }
