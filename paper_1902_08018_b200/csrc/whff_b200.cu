@@ -951,12 +951,37 @@ __global__ void k_blocked_finish(const double* part, uint64_t rows, uint64_t nse
   }
 }
 
+// First non-finite element (mpgemv.py:42-51, codec.py:312-313): grid-stride
+// over float4 with four streaming loads in flight per thread; the minimum
+// index over threads via atomicMin.
 __global__ void k_find_nonfinite(const float* x, uint64_t n, unsigned long long* status) {
-  const uint64_t stride = (uint64_t)gridDim.x * blockDim.x;
+  const uint64_t tid = blockIdx.x * (uint64_t)blockDim.x + threadIdx.x;
+  const uint64_t nt = (uint64_t)gridDim.x * blockDim.x;
   unsigned long long bad = ~0ull;
-  for (uint64_t i = blockIdx.x * (uint64_t)blockDim.x + threadIdx.x; i < n; i += stride) {
-    if (!isfinite(ldg(x + i))) { bad = i; break; }
+  auto nonfinite = [](float f) { return (__float_as_uint(f) & 0x7F800000u) == 0x7F800000u; };
+  uint64_t j0 = 0;
+  if ((reinterpret_cast<uintptr_t>(x) & 15u) == 0) {
+    const float4* x4 = reinterpret_cast<const float4*>(x);
+    const uint64_t n4 = n / 4;
+    for (uint64_t q = tid; q < n4 && bad == ~0ull; q += 4 * nt) {
+      float4 a[4];
+#pragma unroll
+      for (int u = 0; u < 4; ++u) {
+        const uint64_t k = q + u * nt;
+        a[u] = k < n4 ? __ldcs(x4 + k) : make_float4(0.f, 0.f, 0.f, 0.f);
+      }
+#pragma unroll
+      for (int u = 0; u < 4; ++u) {
+        const float e[4] = {a[u].x, a[u].y, a[u].z, a[u].w};
+#pragma unroll
+        for (int c = 0; c < 4; ++c)
+          if (nonfinite(e[c])) bad = min(bad, (unsigned long long)(4 * (q + u * nt) + c));
+      }
+    }
+    j0 = n4 * 4;
   }
+  for (uint64_t i = j0 + tid; i < n && bad == ~0ull; i += nt)
+    if (nonfinite(ldg(x + i))) bad = i;
   if (bad != ~0ull) atomicMin(status, bad);
 }
 

@@ -78,3 +78,20 @@ def test_plugin_gemv_kernel_matches_compiled_reference(golden):
     k = "g02"
     got = backend.gemv_kernel(g[k + "_m"], g[k + "_v"], "mixed", "fixed-tree", 16)
     assert np.array_equal(got, g[f"{k}_mixed_fixed-tree_16"])
+
+
+def test_find_nonfinite_first_index_any_alignment():
+    """whff_find_nonfinite returns the smallest flat index of a NaN/inf, for
+    aligned (float4 path) and unaligned views (scalar path) alike."""
+    import random
+    import torch
+    from paper_1902_08018_b200.codec import find_nonfinite
+    random.seed(0)
+    for _ in range(120):
+        n = random.randint(1, 5000)
+        off = random.randint(0, 3)
+        y = torch.rand(n + off, device="cuda")[off:]
+        idx = sorted(random.sample(range(n), min(n, random.randint(0, 3))))
+        for i in idx:
+            y[i] = random.choice([float("nan"), float("inf"), float("-inf")])
+        assert find_nonfinite(y) == (idx[0] if idx else None)
