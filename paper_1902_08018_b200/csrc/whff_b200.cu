@@ -249,6 +249,19 @@ __global__ void __launch_bounds__(256) k_decode_words(StreamView s, float* out, 
   float x[16];
   reconstruct_words(d, x);
   const uint64_t r0 = brow * 4, c0 = bcol * 4;
+  // interior blocks of a 16-byte aligned output: one 16-byte store per row
+  const bool full = r0 + 4 <= s.rows && c0 + 4 <= s.cols &&
+                    ((reinterpret_cast<uintptr_t>(out) | (ld * 4)) & 15u) == 0;
+  if (full) {
+#pragma unroll
+    for (int i = 0; i < 4; ++i)
+      *reinterpret_cast<float4*>(out + (r0 + i) * ld + c0) =
+          make_float4(x[4 * i], x[4 * i + 1], x[4 * i + 2], x[4 * i + 3]);
+    uint32_t anybad = 0;
+#pragma unroll
+    for (int k = 0; k < 16; ++k) anybad |= (__float_as_uint(x[k]) & 0x7F800000u) == 0x7F800000u;
+    if (!anybad) return;
+  }
   unsigned long long bad = ~0ull;
 #pragma unroll
   for (int i = 0; i < 4; ++i) {
@@ -258,7 +271,7 @@ __global__ void __launch_bounds__(256) k_decode_words(StreamView s, float* out, 
     for (int j = 0; j < 4; ++j) {
       const uint64_t c = c0 + j;
       if (c < s.cols) {
-        out[r * ld + c] = x[4 * i + j];
+        if (!full) out[r * ld + c] = x[4 * i + j];
         if (!isfinite(x[4 * i + j])) {
           const unsigned long long f = r * s.cols + c;
           bad = f < bad ? f : bad;
