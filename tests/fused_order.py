@@ -18,6 +18,9 @@ bit for bit rather than within the reference's bound:
   binary32 sum ("single").
 
 The decoded matrix must be the codec's bit-exact words (oracle decompress).
+`fused_coefficient` models the coefficient-domain evaluation the same way
+(binary32 FMAs emulated exactly, with a rational fallback for the rare
+binary64 results that land on a binary32 tie).
 """
 
 import numpy as np
@@ -71,3 +74,146 @@ def fused_exact(words, v, policy="mixed"):
     tot = _butterfly(per_vw)                 # (br, 4)
     out = tot.astype(np.float32).reshape(br * 4)[:rows]
     return out
+
+
+# ---------------------------------------------------------------------------
+# coefficient-domain evaluation (EVAL_COEFF)
+# ---------------------------------------------------------------------------
+# G = the real-valued inverse lift (csrc/whff_b200.cu c_G); SEQ = raster
+# position of the i-th coefficient in sequency order (codec.py:40).
+G = np.array([[1.0, 1.5, -1.0, -0.25],
+              [1.0, 0.5, 1.0, 1.25],
+              [1.0, -0.5, 1.0, -1.25],
+              [1.0, -1.5, -1.0, 0.25]], np.float32)
+SEQ = [0, 1, 4, 2, 5, 8, 3, 6, 9, 12, 7, 10, 13, 11, 14, 15]
+EMAX_BIAS, QUANT_BITS = 160, 26
+
+
+def _round_f32(x):
+    """Correctly rounded binary32 of a Fraction (ties to even)."""
+    from fractions import Fraction
+    c = np.float32(float(x))
+    best = None
+    for cand in (np.nextafter(c, np.float32(-np.inf)), c, np.nextafter(c, np.float32(np.inf))):
+        err = abs(Fraction(float(cand)) - x)
+        key = (err, int(cand.view(np.uint32)) & 1)
+        if best is None or key < best[0]:
+            best = (key, cand)
+    return best[1]
+
+
+def fma32(a, b, c):
+    """Elementwise binary32 fma(a, b, c), exactly rounded."""
+    from fractions import Fraction
+    a, b, c = np.broadcast_arrays(*(np.atleast_1d(np.asarray(t, np.float32)) for t in (a, b, c)))
+    r = a.astype(np.float64) * b.astype(np.float64) + c.astype(np.float64)   # a*b exact
+    out = r.astype(np.float32)
+    f = out.astype(np.float64)
+    toward = np.where(r > f, np.float32(np.inf), np.float32(-np.inf)).astype(np.float32)
+    mid = (f + np.nextafter(out, toward).astype(np.float64)) / 2
+    amb = (r == mid) & (r != f)            # binary64 rounding landed on a binary32 tie
+    for idx in zip(*np.nonzero(amb)):
+        out[idx] = _round_f32(Fraction(float(a[idx])) * Fraction(float(b[idx]))
+                              + Fraction(float(c[idx])))
+    return out
+
+
+def fma64(a, b, c):
+    """Scalar binary64 fma, exactly rounded."""
+    from fractions import Fraction
+    return float(Fraction(float(a)) * Fraction(float(b)) + Fraction(float(c)))
+
+
+def fused_coefficient(orc, stream, v, policy="mixed"):
+    """Rows of the coefficient-domain evaluation in the fused kernel's order,
+    from the oracle's decode_blocks fields of a host stream."""
+    v = np.asarray(v, np.float32)
+    rows, cols = stream.rows, stream.cols
+    code, _ = orc.mode_kind(stream.mode)
+    payload = np.ascontiguousarray(stream.payload, np.uint8)
+    index = np.ascontiguousarray(stream.block_index, np.uint64)
+    seg = orc.segment_lengths(stream.mode, payload.size, index)
+    mag, neg, emax, raw, raw_words, _ = orc.decode_blocks(
+        payload, index, seg, 27, orc.planes_limit_for(stream.mode), code == 2)
+    words = orc.decompress(stream)
+    bc = (cols + 3) // 4
+    br = (rows + 3) // 4
+    gpr = (bc + 31) // 32
+    nbp = gpr * 32
+    # per block-column u = G^T v (binary64 sum, binary32 result; k_coeff_prep)
+    vp = np.zeros(nbp * 4, np.float32)
+    vp[:cols] = v
+    V = vp.reshape(nbp, 4)
+    U = np.zeros((nbp, 4), np.float32)
+    for k in range(4):
+        t = np.zeros(nbp, np.float64)
+        for j in range(4):
+            t = t + np.float64(G[j, k]) * V[:, j].astype(np.float64)
+        U[:, k] = t.astype(np.float32)
+    # per-block fields, padded to (br, nbp)
+    def pad(a, fill=0):
+        out = np.full((br, nbp) + a.shape[1:], fill, a.dtype)
+        out[:, :bc] = a.reshape((br, bc) + a.shape[1:])
+        return out
+    mag, neg, emax, raw = pad(mag), pad(neg), pad(emax), pad(raw)
+    k = emax.astype(np.int64) - EMAX_BIAS - QUANT_BITS
+    ok = (raw == 0) & ((emax == 0) | ((k >= -126) & (k <= 100)))
+    use = ok & (emax != 0)
+    # sink: w[a] = fma(q, u[j], w[a]) over significant coefficients in order
+    w = np.zeros((br, nbp, 4), np.float32)
+    for c in range(16):
+        pos = SEQ[c]
+        a, j = pos >> 2, pos & 3
+        q = mag[:, :, c].astype(np.float32)
+        q = np.where(neg[:, :, c] != 0, -q, q).astype(np.float32)
+        sig = mag[:, :, c] != 0
+        nw = fma32(q, np.broadcast_to(U[None, :, j], q.shape), w[:, :, a])
+        w[:, :, a] = np.where(sig, nw, w[:, :, a])
+    sc = np.zeros((br, nbp), np.float32)
+    kk = np.clip(k, -126, 100)
+    sc[:] = np.ldexp(np.float32(1.0), kk).astype(np.float32)
+    T = (w * sc[:, :, None]).astype(np.float32)               # exact scaling (or underflow RN)
+    # fallback blocks: exact spatial products (raw escapes, extreme scales)
+    fb = ~ok & ((raw != 0) | (emax != 0))
+    Xp = np.zeros((br * 4, nbp * 4), np.float32)
+    Xp[:rows, :cols] = words
+    X = Xp.reshape(br, 4, nbp, 4).transpose(0, 2, 1, 3)       # [br, bcol, i, j]
+    single = policy == "single"
+    acc_t = np.float32 if single else np.float64
+    Pf = (X * V[None, :, None, :]).astype(np.float32)          # binary32 products
+    # lane accumulation: vw over groups, blocks = 32 lanes of a group
+    D = np.zeros((br, 32, 32, 4), acc_t)                       # [br, vw, lane, a]
+    R = np.zeros((br, 32, 32, 4), acc_t)                       # [br, vw, lane, i]
+    nk = (gpr + 31) // 32
+    for kq in range(nk):
+        for vw in range(32):
+            g = vw + 32 * kq
+            if g >= gpr:
+                continue
+            sl = slice(32 * g, 32 * g + 32)
+            t = T[:, sl, :].astype(acc_t)
+            D[:, vw] = np.where(use[:, sl, None], D[:, vw] + t, D[:, vw])
+            m = fb[:, sl]
+            for i in range(4):
+                r = R[:, vw, :, i]
+                for jj in range(4):
+                    r = np.where(m, r + Pf[:, sl, i, jj].astype(acc_t), r)
+                R[:, vw, :, i] = r
+    Dv = _butterfly(np.moveaxis(D, 2, -1))                     # [br, vw, a]
+    Rv = _butterfly(np.moveaxis(R, 2, -1))                     # [br, vw, i]
+    Dt = _butterfly(np.moveaxis(Dv, 1, -1))                    # [br, a]
+    Rt = _butterfly(np.moveaxis(Rv, 1, -1))                    # [br, i]
+    out = np.zeros(br * 4, np.float32)
+    for b in range(br):
+        for i in range(4):
+            if single:
+                t = np.float32(Rt[b, i])
+                for a in range(4):
+                    t = fma32(G[i, a], Dt[b, a], t)[0]
+                out[4 * b + i] = t
+            else:
+                t = float(Rt[b, i])
+                for a in range(4):
+                    t = fma64(G[i, a], Dt[b, a], t)
+                out[4 * b + i] = np.float32(t)
+    return out[:rows]

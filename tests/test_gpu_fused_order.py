@@ -1,6 +1,7 @@
-"""The exact fused evaluation, bit for bit, against a CPU model of its
-summation order (tests/fused_order.py) applied to the oracle's decoded words:
-every policy, stream variant and layout, ragged shapes, raw escapes."""
+"""Both fused evaluations, bit for bit, against CPU models of their
+arithmetic and summation order (tests/fused_order.py) applied to the
+oracle's decoded words / fields: every policy, stream variant and layout,
+ragged shapes, raw escapes and extreme scales."""
 
 import numpy as np
 import pytest
@@ -43,4 +44,32 @@ def test_exact_matches_order_model(orc, kind, rows, cols, mode_kind, param, layo
     for policy in ("mixed", "single", "double"):
         got = ds.gemv(vd, policy=policy, evaluation="exact").cpu().numpy()
         want = fused_exact(words, v, policy)
+        assert np.array_equal(got.view(np.uint32), want.view(np.uint32)), (policy, kind, mode_kind)
+
+
+@pytest.mark.parametrize("kind,rows,cols", [("smooth", 37, 20011), ("noise", 23, 4099),
+                                            ("noise", 5, 3)])
+@pytest.mark.parametrize("mode_kind,param", [("rate", 8), ("precision", 17), ("accuracy", 1e-12)])
+@pytest.mark.parametrize("layout", ["reference", "skeleton-first"])
+def test_coefficient_matches_order_model(orc, kind, rows, cols, mode_kind, param, layout, rng):
+    """The coefficient-domain evaluation (bench default), bit for bit, against
+    tests/fused_order.fused_coefficient on the oracle's decoded fields: u = G^T v
+    per block column, binary32 FMAs in coefficient order, 2^k scaling, binary64
+    lane sums, the exact spatial fallback for raw / extreme blocks, the two
+    butterflies and the final G combination."""
+    import torch
+    from fused_order import fused_coefficient
+    from paper_1902_08018_b200 import codec
+    mode = {"rate": codec.FixedRate, "precision": codec.FixedPrecision,
+            "accuracy": codec.FixedAccuracy}[mode_kind](param)
+    C = matrix(kind, rows, cols, rng)
+    host = codec.compress(C, mode)
+    ds = codec.DeviceStream.from_host(host)
+    if layout != "reference":
+        ds.relayout(layout)
+    v = rng.random(cols).astype(np.float32)
+    vd = torch.from_numpy(v).cuda()
+    for policy in ("mixed", "single"):
+        got = ds.gemv(vd, policy=policy, evaluation="coefficient").cpu().numpy()
+        want = fused_coefficient(orc, host, v, policy)
         assert np.array_equal(got.view(np.uint32), want.view(np.uint32)), (policy, kind, mode_kind)
