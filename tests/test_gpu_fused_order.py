@@ -73,3 +73,20 @@ def test_coefficient_matches_order_model(orc, kind, rows, cols, mode_kind, param
         got = ds.gemv(vd, policy=policy, evaluation="coefficient").cpu().numpy()
         want = fused_coefficient(orc, host, v, policy)
         assert np.array_equal(got.view(np.uint32), want.view(np.uint32)), (policy, kind, mode_kind)
+
+
+def test_paper_width_rows_match_order_models(orc, rng):
+    """Paper slit width (256,000 columns: 2,000 groups, 63 per virtual warp),
+    FixedRate(8), skeleton-first: both evaluations bit-exact vs the models."""
+    import torch
+    from fused_order import fused_coefficient
+    from paper_1902_08018_b200 import codec
+    C = matrix("smooth", 40, 256000, rng)
+    host = codec.compress(C, codec.FixedRate(8))
+    ds = codec.DeviceStream.from_host(host).relayout("skeleton-first")
+    v = rng.random(256000).astype(np.float32)
+    vd = torch.from_numpy(v).cuda()
+    got = ds.gemv(vd, evaluation="coefficient").cpu().numpy()
+    assert np.array_equal(got.view(np.uint32), fused_coefficient(orc, host, v).view(np.uint32))
+    got = ds.gemv(vd, evaluation="exact").cpu().numpy()
+    assert np.array_equal(got.view(np.uint32), fused_exact(orc.decompress(host), v).view(np.uint32))
