@@ -25,3 +25,22 @@ def test_within_reference_bound(orc, rng):
     ref = np.asarray(orc.gemv_kernel(m, v, "mixed", "sequential"), np.float64)
     bound = (m.shape[1] + 1) * np.finfo(np.float32).eps * (np.abs(m).astype(np.float64) @ v)
     assert (np.abs(got - ref) <= bound).all()
+
+
+def test_coefficient_model_within_reference_bound_smooth(orc, rng):
+    """The coefficient-domain model on a smooth operator (the WHFF case)
+    stays inside the reference's per-row bound around the sequential GEMV of
+    the decoded words (DESIGN §2 tolerance contract)."""
+    from fused_order import fused_coefficient
+    from paper_1902_08018_b200 import codec, synth
+    spec = synth.Spec(grid_rows=16, grid_cols=16, S=6001, K=13, M=13, seed=4)
+    C = synth.deformation_rows(spec, 2, 0.9, 0, 13)
+    for mode in (codec.FixedRate(8), codec.FixedAccuracy(1e-12)):
+        host = orc.compress(C, mode)
+        host.mode = mode
+        words = orc.decompress(host)
+        v = rng.random(C.shape[1]).astype(np.float32)
+        got = fused_coefficient(orc, host, v).astype(np.float64)
+        ref = np.asarray(orc.gemv_kernel(words, v, "mixed", "sequential"), np.float64)
+        bound = (C.shape[1] + 1) * np.finfo(np.float32).eps * (np.abs(words).astype(np.float64) @ v)
+        assert (np.abs(got - ref) <= bound).all()
