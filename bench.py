@@ -528,9 +528,11 @@ def b200_main(args, world, rank, local):
                     and e.get("slits", 52) == args.slits and e.get("S", 256000) == args.S):
                 traffic = e.get("dram_bytes_per_launch")
                 if "thread_instr_per_block" in e:
-                    # instruction roofline: the SM issue budget per 16-byte
-                    # block at HBM speed is 128 lane-instr/clk * clk / (blocks/s at peak)
-                    budget = 128 * 148 * 1.965e9 / (hbm * 1e9 / 16)
+                    # instruction roofline: the SM issue budget per block
+                    # at HBM speed is 128 lane-instr/clk * clk / (blocks/s at peak);
+                    # a block is 16 bytes at FixedRate(8), fewer in variable modes
+                    bpb = kernel_bytes / e.get("blocks_per_launch", kernel_bytes / 16)
+                    budget = 128 * 148 * 1.965e9 / (hbm * 1e9 / bpb)
                     instr = {"thread_instr_per_block": e["thread_instr_per_block"],
                              "budget_at_hbm_peak": round(budget, 1),
                              "alu_pipe_pct": e.get("alu_pipe_pct"),
