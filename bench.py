@@ -47,9 +47,11 @@ def parse():
                     help="coefficient: accumulate 2^k Q (G^T v) per block and apply the inverse "
                          "lift G once per block-row (SURVEY 7, hard part 2); exact: decoded "
                          "binary32 words x v, the reference's products")
-    ap.add_argument("--layout", default="skeleton-first", choices=["reference", "skeleton-first"],
-                    help="device payload layout (whff_dstream_relayout): a per-block bit "
-                         "permutation of the WHFZ stream, same bytes, same decoded words")
+    ap.add_argument("--layout", default="packed", choices=["reference", "skeleton-first", "packed"],
+                    help="packed: the tile-packed device copy (whff_dstream_pack: the decoded "
+                         "coefficients as fixed-width fields per segment, bit-exact words) is "
+                         "what the kernel reads; reference / skeleton-first: the fused kernel "
+                         "parses the WHFZ bitstream (or its per-block bit permutation) itself")
     ap.add_argument("--policy", default="mixed", choices=["mixed", "single", "double"])
     ap.add_argument("--slits", type=int, default=52)
     ap.add_argument("--rows", type=int, default=378)
@@ -185,7 +187,9 @@ def build_field(args, world, rank):
             rows = synth.deformation_rows(spec, a, ops.phases[synth.AXES[a]], src * args.rows,
                                           (src + 1) * args.rows, device="cuda")
             made[(a, src)] = codec.compress_device(rows, mode)
-            if args.layout != "reference":
+            if args.layout == "packed":
+                made[(a, src)].pack()
+            elif args.layout != "reference":
                 made[(a, src)].relayout(args.layout)
             del rows
             streams[a][src] = made[(a, src)]
@@ -203,15 +207,24 @@ def build_field(args, world, rank):
     # compressed bytes this rank decodes per step: the block-rows of its jobs
     # (a slit split across two ranks is held by both but decoded once)
     stream_bytes = 0
+    packed_bytes, exceptions, blocks = 0, 0, 0
     for a, s_, r0, r1 in jobs:
         ds = streams[a][s_]
         nbr = (r1 + 3) // 4 - r0 // 4
         stream_bytes += (ds.payload_bytes + ds.index_bytes) * nbr / ds.block_rows
+        if getattr(ds, "packed", False):
+            packed_bytes += ds.packed_bytes * nbr / ds.block_rows
+            exceptions += ds.packed_exceptions
+        blocks += nbr * ds.block_cols
     stream_bytes = int(round(stream_bytes))
     info = {"t_ops_s": round(t_ops, 2), "t_encode_s": round(t_enc, 2),
             "streams": sum(1 for row in streams for ds in row if ds is not None),
             "distinct_per_axis": distinct, "stream_bytes_rank": stream_bytes,
-            "index_kind": streams[need[0][0]][need[0][1]].index_kind if need else None}
+            "index_kind": streams[need[0][0]][need[0][1]].index_kind if need else None,
+            "packed_bytes_rank": int(round(packed_bytes)),
+            "packed_bits_per_block": round(8 * packed_bytes / max(blocks, 1), 2),
+            "reference_bits_per_block": round(8 * stream_bytes / max(blocks, 1), 2),
+            "packed_exceptions": exceptions}
     return fs, spec, ops, mode, streams, info
 
 
@@ -572,7 +585,13 @@ def b200_main(args, world, rank, local):
                 "ms_per_step": round(e2e_ms, 4), "h2d_bytes_per_step": T * 4,
                 "d2h_bytes_per_step": out_rows * 4},
         "gpu_launches": launches_per_step * args.steps,
-        "roofline": {"bound": "hbm", "kernel": "k_decode_gemv", "achieved": round(achieved, 2),
+        "roofline": {"bound": "hbm", "kernel": "k_pk_gemv" if args.layout == "packed" else "k_decode_gemv",
+                     "bytes": ("tile-packed copy read by the launch (body + segment headers + "
+                               "exception list) + vector + output" if args.layout == "packed" else
+                               "WHFZ payload + device index + vector + output"),
+                     "reference_stream_gbs": round(job_bytes / (kernel_ms / 1e3) / 1e9, 2),
+                     "reference_stream_frac": round(job_bytes / (kernel_ms / 1e3) / 1e9 / hbm, 4),
+                     "achieved": round(achieved, 2),
                      "peak": hbm, "peak_kind": f"{pk_kind} hbm_gbs (burst copy)", "unit": "GB/s",
                      "frac": round(achieved / hbm, 4), "traffic": traffic,
                      "bytes_per_launch": int(kernel_bytes), "kernel_ms": round(kernel_ms, 4),

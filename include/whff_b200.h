@@ -40,7 +40,7 @@
 extern "C" {
 #endif
 
-#define WHFF_ABI_VERSION 1
+#define WHFF_ABI_VERSION 2
 #define WHFF_STATUS_CLEAR UINT64_MAX
 
 typedef struct CUstream_st* whff_stream_t; /* == cudaStream_t */
@@ -99,6 +99,10 @@ typedef struct whff_dstream_info {
   int32_t planes_limit;
   int32_t has_raw_flag;
   int32_t layout;          /* whff_layout_t */
+  int32_t packed;          /* 1: the tile-packed copy exists (whff_dstream_pack) */
+  uint64_t packed_bytes;   /* bytes of the packed copy a full GEMV reads      */
+  uint64_t packed_exceptions; /* blocks held as exact words in its side list   */
+  int32_t device;          /* CUDA device the stream's memory lives on          */
 } whff_dstream_info_t;
 
 int whff_abi_version(void);
@@ -132,6 +136,21 @@ whff_status_t whff_dstream_destroy(whff_dstream_t s);
  * every block segment, computed by the reference parse on the device).
  * Needs an implicit or compact index (disjoint segments).  Synchronous.    */
 whff_status_t whff_dstream_relayout(whff_dstream_t s, int layout, whff_stream_t stream);
+/* Build the stream's tile-packed device copy (csrc/whff_packed.cuh): the
+ * decoded coefficients of every block -- exactly the fields decode_blocks
+ * (K:371-408) yields -- re-coded losslessly as fixed-width fields per
+ * 4-block-row x 256-block-column segment, plus an exact-word side list for
+ * raw-escape / extreme-scale blocks.  Decoded words stay bit-exact; every
+ * decode / decode_gemv / plan call on a packed stream reads the packed copy
+ * (the WHFZ payload stays for download, decode_blocks and relayout).  A
+ * rebind / import drops it.  Synchronous on `stream`.                     */
+whff_status_t whff_dstream_pack(whff_dstream_t s, whff_stream_t stream);
+/* The packed copy to host memory (tooling / tests): segment headers (48 B
+ * each), body words, exception block indices and words (16 u32 each).
+ * NULL buffers: only the counts are returned.  Synchronous.               */
+whff_status_t whff_dstream_packed_download(whff_dstream_t s, uint8_t* segs_host, uint32_t* body_host,
+                                           uint64_t* exc_block_host, uint32_t* exc_words_host,
+                                           uint64_t* n_segs, uint64_t* body_words, uint64_t* n_exc);
 /* Physically distinct device copy of a stream (same device).  Synchronous. */
 whff_status_t whff_dstream_clone(whff_dstream_t s, whff_dstream_t* out);
 whff_status_t whff_dstream_get_info(whff_dstream_t s, whff_dstream_info_t* info);

@@ -34,7 +34,9 @@ class DStreamInfo(ctypes.Structure):
                 ("payload_bytes", ctypes.c_uint64), ("total_bits", ctypes.c_uint64),
                 ("index_bytes", ctypes.c_uint64),
                 ("device_bytes", ctypes.c_uint64), ("planes_limit", ctypes.c_int32),
-                ("has_raw_flag", ctypes.c_int32), ("layout", ctypes.c_int32)]
+                ("has_raw_flag", ctypes.c_int32), ("layout", ctypes.c_int32),
+                ("packed", ctypes.c_int32), ("packed_bytes", ctypes.c_uint64),
+                ("packed_exceptions", ctypes.c_uint64), ("device", ctypes.c_int32)]
 
 
 _P = ctypes.c_void_p
@@ -49,6 +51,8 @@ _SIG = {
     "whff_dstream_destroy": ([_P], _I),
     "whff_dstream_clone": ([_P, _P], _I),
     "whff_dstream_relayout": ([_P, _I, _P], _I),
+    "whff_dstream_pack": ([_P, _P], _I),
+    "whff_dstream_packed_download": ([_P, _P, _P, _P, _P, _P, _P, _P], _I),
     "whff_dstream_get_info": ([_P, _P], _I),
     "whff_dstream_download": ([_P, _P, _P], _I),
     "whff_dstream_export": ([_P, _P, _P, _P, _P], _I),

@@ -156,7 +156,16 @@ class DeviceStream:
         self.layout = _lib.LAYOUT_NAME[int(info.layout)]
         self.total_bits = total_bits if total_bits is not None else int(info.total_bits)
         import torch
-        self.device = torch.device("cuda", torch.cuda.current_device())
+        self.device = torch.device("cuda", int(info.device))
+        self._refresh()
+
+    def _refresh(self):
+        info = _lib.DStreamInfo()
+        _lib.call("whff_dstream_get_info", self._h, ctypes.byref(info))
+        self.packed = bool(info.packed)
+        self.packed_bytes = int(info.packed_bytes)
+        self.packed_exceptions = int(info.packed_exceptions)
+        self.device_bytes = int(info.device_bytes)
 
     @property
     def handle(self):
@@ -204,6 +213,14 @@ class DeviceStream:
         self.layout = layout
         return self
 
+    def pack(self):
+        """Build the tile-packed device copy (whff_dstream_pack; csrc/whff_packed.cuh):
+        the decoded coefficients re-coded losslessly as fixed-width fields per
+        segment -- decode / gemv / plans then read it (words stay bit-exact)."""
+        _lib.call("whff_dstream_pack", self._h, _lib.cur_stream())
+        self._refresh()
+        return self
+
     def clone(self):
         """A physically distinct HBM copy (whff_dstream_clone)."""
         h = ctypes.c_void_p()
@@ -238,6 +255,7 @@ class DeviceStream:
         """Set the payload size alone (for plans built before the bytes arrive)."""
         _lib.call("whff_dstream_rebind", self._h, int(payload_bytes))
         self.payload_bytes = int(payload_bytes)
+        self._refresh()
 
     def import_async(self, payload, index):
         """Rebind to a same-geometry stream's exported contents (async H2D on
@@ -245,6 +263,7 @@ class DeviceStream:
         _lib.call("whff_dstream_import_async", self._h, _lib.ptr(payload), int(payload.numel()),
                   _lib.ptr(index) if index.numel() else None, int(index.numel()), _lib.cur_stream())
         self.payload_bytes = int(payload.numel())
+        self._refresh()
 
     # -- device operations -------------------------------------------------
     def decode(self, out=None, check=True):
@@ -306,7 +325,11 @@ class DeviceStream:
 
 
 def to_device(stream, device=None, layout="reference"):
+    """Upload (if needed) and lay out: "reference" / "skeleton-first" permute
+    the WHFZ payload; "packed" adds the tile-packed copy the kernels read."""
     ds = stream if isinstance(stream, DeviceStream) else DeviceStream.from_host(stream, device)
+    if layout == "packed":
+        return ds.pack()
     if layout != ds.layout:
         ds.relayout(layout)
     return ds

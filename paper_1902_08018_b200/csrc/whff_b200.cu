@@ -25,8 +25,8 @@
 #include "whff_decode.cuh"
 #include "whff_encode.cuh"
 #include "whff_relayout.cuh"
-
-using namespace whff;
+#include "whff_common.cuh"
+#include "whff_packed_api.h"
 
 // ---------------------------------------------------------------------------
 // error plumbing
@@ -55,23 +55,6 @@ whff_status_t cuda_fail(cudaError_t e, const char* what) {
     if (e_ != cudaSuccess) return cuda_fail(e_, what);     \
   } while (0)
 
-// ---------------------------------------------------------------------------
-// device view of a stream
-// ---------------------------------------------------------------------------
-struct StreamView {
-  const uint32_t* words;     // payload as LE uint32 words (padded)
-  const uint64_t* base;      // COMPACT: start bit of block (br, 32g)
-  const uint16_t* lens;      // COMPACT/FULL: segment bits (clamped 65535)
-  const uint64_t* starts;    // FULL: start bit per block
-  uint64_t payload_bits;
-  uint64_t rows, cols, br, bc, gpr;
-  uint32_t seg_bits;         // IMPLICIT: 16 * bpv
-  int32_t kind;
-  int32_t planes_limit;
-  int32_t has_raw;
-  int32_t layout;
-};
-
 struct whff_dstream {
   int device;
   int mode;
@@ -87,6 +70,14 @@ struct whff_dstream {
   uint16_t* d_lens = nullptr;
   uint64_t* d_starts = nullptr;
   size_t index_bytes = 0;
+  // tile-packed representation (whff_dstream_pack; whff_packed.cuh)
+  bool packed = false;
+  uint32_t* d_pk_body = nullptr;
+  pk::Seg* d_pk_segs = nullptr;
+  uint64_t* d_pk_exc_block = nullptr;
+  uint32_t* d_pk_exc_words = nullptr;
+  uint64_t pk_body_words = 0, pk_nexc = 0, pk_alloc_words = 0;
+  std::vector<uint64_t> pk_band_bytes;   // bytes a GEMV reads per band (body + headers + exceptions)
 
   StreamView view() const {
     StreamView v;
@@ -108,42 +99,6 @@ struct whff_dstream {
     return v;
   }
 };
-
-__device__ __forceinline__ int clamp_len(uint64_t start, uint64_t seg, uint64_t payload_bits) {
-  if (start >= payload_bits) return 0;
-  uint64_t lim = start + seg;
-  if (lim > payload_bits) lim = payload_bits;
-  const uint64_t l = lim - start;
-  return l > 65535u ? 65535 : (int)l;
-}
-
-// start/len of one block, any index kind (COMPACT walks <= 31 lengths)
-__device__ void block_extent(const StreamView& s, uint64_t b, uint64_t& start, int& len) {
-  if (s.kind == WHFF_INDEX_IMPLICIT) {
-    start = b * (uint64_t)s.seg_bits;
-    len = clamp_len(start, s.seg_bits, s.payload_bits);
-  } else if (s.kind == WHFF_INDEX_FULL) {
-    start = s.starts[b];
-    len = clamp_len(start, s.lens[b], s.payload_bits);
-  } else {
-    const uint64_t brow = b / s.bc, bcol = b % s.bc;
-    const uint64_t g0 = bcol & ~31ull;
-    uint64_t st = s.base[brow * s.gpr + (bcol >> 5)];
-    for (uint64_t c = g0; c < bcol; ++c) st += s.lens[brow * s.bc + c];
-    start = st;
-    len = clamp_len(start, s.lens[b], s.payload_bits);
-  }
-}
-
-// either layout, refill path, for the thread-per-block kernels
-template <bool HAS_RAW>
-__device__ __forceinline__ void decode_any(const StreamView& s, BitWin& bw, int planes_limit,
-                                           Decoded& d) {
-  if (s.layout == WHFF_LAYOUT_SKELETON_FIRST)
-    decode_block_sf<HAS_RAW, true>(bw, planes_limit, d);
-  else
-    decode_block<HAS_RAW, true>(bw, planes_limit, d, __activemask());
-}
 
 // ---------------------------------------------------------------------------
 // decode_blocks parity hook (K:371-408)
@@ -315,25 +270,6 @@ struct JobTable {
   unsigned* tickets;         // [block-row] warp arrival counters (zero between launches)
 };
 
-// G = real-valued inverse lift (codec.py:128-134 with >>1 -> /2, <<1 -> *2);
-// the decoded block is 2^(e-26) * G Q G^T up to lift rounding.
-__device__ __constant__ float c_G[4][4] = {{1.0f, 1.5f, -1.0f, -0.25f},
-                                          {1.0f, 0.5f, 1.0f, 1.25f},
-                                          {1.0f, -0.5f, 1.0f, -1.25f},
-                                          {1.0f, -1.5f, -1.0f, 0.25f}};
-
-// block-column vector slice, zero padded past cols
-__device__ __forceinline__ float4 load_v4(const float* v, uint64_t bcol, uint64_t cols, bool aligned) {
-  const uint64_t c0 = bcol * 4;
-  if (aligned && c0 + 3 < cols) return ldg(reinterpret_cast<const float4*>(v) + bcol);
-  float4 r;
-  r.x = c0 + 0 < cols ? ldg(v + c0 + 0) : 0.0f;
-  r.y = c0 + 1 < cols ? ldg(v + c0 + 1) : 0.0f;
-  r.z = c0 + 2 < cols ? ldg(v + c0 + 2) : 0.0f;
-  r.w = c0 + 3 < cols ? ldg(v + c0 + 3) : 0.0f;
-  return r;
-}
-
 // Accumulators for the three policies (mpgemv.py:1-7):
 //   mixed : binary32 product, binary64 sum     single: binary32 both
 //   double: binary64 product and sum
@@ -441,7 +377,6 @@ constexpr int kGemvWarps = 8;
 // 285 rows) still fill the GPU; the last of the row's warps to finish adds
 // the kVW partials with another fixed butterfly.  The order is fixed, so a
 // row's result does not depend on the launch that computes it.
-constexpr int kVW = 32;
 constexpr int kSplit = kVW / kGemvWarps;   // CTAs per block-row
 
 // Software-pipelined segment location for indexed / implicit variable-rate
@@ -1195,7 +1130,37 @@ void free_stream(whff_dstream* s) {
   cudaFree(s->d_base);
   cudaFree(s->d_lens);
   cudaFree(s->d_starts);
+  cudaFree(s->d_pk_body);
+  cudaFree(s->d_pk_segs);
+  cudaFree(s->d_pk_exc_block);
+  cudaFree(s->d_pk_exc_words);
   delete s;
+}
+
+void drop_packed(whff_dstream* s) {
+  if (!s->packed) return;
+  DeviceGuard g(s->device);
+  cudaFree(s->d_pk_body);
+  cudaFree(s->d_pk_segs);
+  cudaFree(s->d_pk_exc_block);
+  cudaFree(s->d_pk_exc_words);
+  s->d_pk_body = nullptr;
+  s->d_pk_segs = nullptr;
+  s->d_pk_exc_block = nullptr;
+  s->d_pk_exc_words = nullptr;
+  s->packed = false;
+  s->pk_body_words = s->pk_nexc = s->pk_alloc_words = 0;
+  s->pk_band_bytes.clear();
+}
+
+PkView pk_view(const whff_dstream* s) {
+  PkView v;
+  v.body = s->d_pk_body;
+  v.segs = s->d_pk_segs;
+  v.exc_block = s->d_pk_exc_block;
+  v.exc_words = s->d_pk_exc_words;
+  v.g = pk::make_geom(s->rows, s->cols);
+  return v;
 }
 
 }  // namespace
@@ -1386,6 +1351,105 @@ whff_status_t whff_dstream_relayout(whff_dstream_t s, int layout, whff_stream_t 
   return WHFF_OK;
 }
 
+// Build the tile-packed representation (whff_packed.cuh) from the stream's
+// payload: pass 1 sizes every segment, two scans place them, pass 2 writes
+// records and exceptions.  Synchronous on `stream`.
+whff_status_t whff_dstream_pack(whff_dstream_t s, whff_stream_t stream) {
+  if (!s) return fail(WHFF_ERR_ARGUMENT, "null stream");
+  if (s->packed) return WHFF_OK;
+  DeviceGuard g(s->device);
+  cudaStream_t cs = (cudaStream_t)stream;
+  const pk::Geom gg = pk::make_geom(s->rows, s->cols);
+  const uint64_t nseg = gg.nband * gg.nsegb;
+  pk::Seg* segs = nullptr;
+  uint64_t *words = nullptr, *exc = nullptr, *off = nullptr, *eoff = nullptr;
+  void* tmp = nullptr;
+  size_t tmp_bytes = 0, t2 = 0;
+  cudaError_t e = cudaMalloc(&segs, nseg * sizeof(pk::Seg));
+  if (e == cudaSuccess) e = cudaMalloc(&words, (nseg + 1) * 8);
+  if (e == cudaSuccess) e = cudaMalloc(&exc, (nseg + 1) * 8);
+  if (e == cudaSuccess) e = cudaMalloc(&off, (nseg + 1) * 8);
+  if (e == cudaSuccess) e = cudaMalloc(&eoff, (nseg + 1) * 8);
+  if (e == cudaSuccess) e = cudaMemsetAsync(words + nseg, 0, 8, cs);
+  if (e == cudaSuccess) e = cudaMemsetAsync(exc + nseg, 0, 8, cs);
+  auto cleanup = [&]() {
+    cudaFree(words);
+    cudaFree(exc);
+    cudaFree(off);
+    cudaFree(eoff);
+    cudaFree(tmp);
+  };
+  if (e != cudaSuccess) { cleanup(); cudaFree(segs); return cuda_fail(e, "pack alloc"); }
+  const StreamView v = s->view();
+  e = pk_launch_stats(v, gg, segs, words, exc, cs);
+  if (e == cudaSuccess) e = cub::DeviceScan::ExclusiveSum(nullptr, tmp_bytes, words, off, (int)(nseg + 1), cs);
+  if (e == cudaSuccess) e = cub::DeviceScan::ExclusiveSum(nullptr, t2, exc, eoff, (int)(nseg + 1), cs);
+  tmp_bytes = std::max(tmp_bytes, t2);
+  if (e == cudaSuccess) e = cudaMalloc(&tmp, tmp_bytes);
+  if (e == cudaSuccess) e = cub::DeviceScan::ExclusiveSum(tmp, tmp_bytes, words, off, (int)(nseg + 1), cs);
+  if (e == cudaSuccess) e = cub::DeviceScan::ExclusiveSum(tmp, tmp_bytes, exc, eoff, (int)(nseg + 1), cs);
+  uint64_t tot[2] = {0, 0};
+  if (e == cudaSuccess) e = cudaMemcpyAsync(&tot[0], off + nseg, 8, cudaMemcpyDeviceToHost, cs);
+  if (e == cudaSuccess) e = cudaMemcpyAsync(&tot[1], eoff + nseg, 8, cudaMemcpyDeviceToHost, cs);
+  if (e == cudaSuccess) e = cudaStreamSynchronize(cs);
+  if (e == cudaSuccess) e = pk_launch_finalize(segs, nseg, off, eoff, cs);
+  // readable slack past the body: rows past a band's end and tails read ahead
+  const uint64_t alloc_words = tot[0] + 4 * pk::kMaxRecordWords * 32 + 64;
+  uint32_t* body = nullptr;
+  uint64_t* xb = nullptr;
+  uint32_t* xw = nullptr;
+  const uint64_t ne = std::max<uint64_t>(tot[1], 1);
+  if (e == cudaSuccess) e = cudaMalloc(&body, alloc_words * 4);
+  if (e == cudaSuccess) e = cudaMemsetAsync(body, 0, alloc_words * 4, cs);
+  if (e == cudaSuccess) e = cudaMalloc(&xb, ne * 8);
+  if (e == cudaSuccess) e = cudaMalloc(&xw, ne * 64);
+  if (e == cudaSuccess) e = pk_launch_emit(v, gg, segs, body, xb, xw, cs);
+  std::vector<uint64_t> hoff(nseg + 1), hexc(nseg + 1);
+  if (e == cudaSuccess) e = cudaMemcpyAsync(hoff.data(), off, (nseg + 1) * 8, cudaMemcpyDeviceToHost, cs);
+  if (e == cudaSuccess) e = cudaMemcpyAsync(hexc.data(), eoff, (nseg + 1) * 8, cudaMemcpyDeviceToHost, cs);
+  if (e == cudaSuccess) e = cudaStreamSynchronize(cs);
+  cleanup();
+  if (e != cudaSuccess) {
+    cudaFree(segs);
+    cudaFree(body);
+    cudaFree(xb);
+    cudaFree(xw);
+    return cuda_fail(e, "pack");
+  }
+  s->d_pk_body = body;
+  s->d_pk_segs = segs;
+  s->d_pk_exc_block = xb;
+  s->d_pk_exc_words = xw;
+  s->pk_body_words = tot[0];
+  s->pk_nexc = tot[1];
+  s->pk_alloc_words = alloc_words;
+  s->pk_band_bytes.assign(gg.nband, 0);
+  for (uint64_t b = 0; b < gg.nband; ++b) {
+    const uint64_t s0 = b * gg.nsegb, s1 = s0 + gg.nsegb;
+    s->pk_band_bytes[b] = (hoff[s1] - hoff[s0]) * 4 + gg.nsegb * sizeof(pk::Seg) + (hexc[s1] - hexc[s0]) * 72;
+  }
+  s->packed = true;
+  return WHFF_OK;
+}
+
+whff_status_t whff_dstream_packed_download(whff_dstream_t s, uint8_t* segs, uint32_t* body, uint64_t* xb,
+                                           uint32_t* xw, uint64_t* n_segs, uint64_t* body_words,
+                                           uint64_t* n_exc) {
+  if (!s) return fail(WHFF_ERR_ARGUMENT, "null stream");
+  if (!s->packed) return fail(WHFF_ERR_ARGUMENT, "stream is not packed (whff_dstream_pack)");
+  const pk::Geom gg = pk::make_geom(s->rows, s->cols);
+  const uint64_t nseg = gg.nband * gg.nsegb;
+  if (n_segs) *n_segs = nseg;
+  if (body_words) *body_words = s->pk_body_words;
+  if (n_exc) *n_exc = s->pk_nexc;
+  DeviceGuard g(s->device);
+  if (segs) WCK(cudaMemcpy(segs, s->d_pk_segs, nseg * sizeof(pk::Seg), cudaMemcpyDeviceToHost));
+  if (body && s->pk_body_words) WCK(cudaMemcpy(body, s->d_pk_body, s->pk_body_words * 4, cudaMemcpyDeviceToHost));
+  if (xb && s->pk_nexc) WCK(cudaMemcpy(xb, s->d_pk_exc_block, s->pk_nexc * 8, cudaMemcpyDeviceToHost));
+  if (xw && s->pk_nexc) WCK(cudaMemcpy(xw, s->d_pk_exc_words, s->pk_nexc * 64, cudaMemcpyDeviceToHost));
+  return WHFF_OK;
+}
+
 whff_status_t whff_dstream_clone(whff_dstream_t s, whff_dstream_t* out) {
   if (!s || !out) return fail(WHFF_ERR_ARGUMENT, "null argument");
   *out = nullptr;
@@ -1395,6 +1459,10 @@ whff_status_t whff_dstream_clone(whff_dstream_t s, whff_dstream_t* out) {
   c->d_base = nullptr;
   c->d_lens = nullptr;
   c->d_starts = nullptr;
+  c->d_pk_body = nullptr;
+  c->d_pk_segs = nullptr;
+  c->d_pk_exc_block = nullptr;
+  c->d_pk_exc_words = nullptr;
   cudaError_t e = cudaMalloc(&c->d_payload, s->payload_alloc);
   if (e == cudaSuccess) e = cudaMemcpy(c->d_payload, s->d_payload, s->payload_alloc, cudaMemcpyDeviceToDevice);
   if (e == cudaSuccess && s->d_base) {
@@ -1408,6 +1476,21 @@ whff_status_t whff_dstream_clone(whff_dstream_t s, whff_dstream_t* out) {
   if (e == cudaSuccess && s->d_starts) {
     e = cudaMalloc(&c->d_starts, s->nb * 8);
     if (e == cudaSuccess) e = cudaMemcpy(c->d_starts, s->d_starts, s->nb * 8, cudaMemcpyDeviceToDevice);
+  }
+  if (e == cudaSuccess && s->packed) {
+    const pk::Geom gg = pk::make_geom(s->rows, s->cols);
+    const uint64_t nseg = gg.nband * gg.nsegb;
+    e = cudaMalloc(&c->d_pk_body, s->pk_alloc_words * 4);
+    if (e == cudaSuccess)
+      e = cudaMemcpy(c->d_pk_body, s->d_pk_body, s->pk_alloc_words * 4, cudaMemcpyDeviceToDevice);
+    if (e == cudaSuccess) e = cudaMalloc(&c->d_pk_segs, nseg * sizeof(pk::Seg));
+    if (e == cudaSuccess)
+      e = cudaMemcpy(c->d_pk_segs, s->d_pk_segs, nseg * sizeof(pk::Seg), cudaMemcpyDeviceToDevice);
+    const uint64_t ne = std::max<uint64_t>(s->pk_nexc, 1);
+    if (e == cudaSuccess) e = cudaMalloc(&c->d_pk_exc_block, ne * 8);
+    if (e == cudaSuccess) e = cudaMemcpy(c->d_pk_exc_block, s->d_pk_exc_block, ne * 8, cudaMemcpyDeviceToDevice);
+    if (e == cudaSuccess) e = cudaMalloc(&c->d_pk_exc_words, ne * 64);
+    if (e == cudaSuccess) e = cudaMemcpy(c->d_pk_exc_words, s->d_pk_exc_words, ne * 64, cudaMemcpyDeviceToDevice);
   }
   if (e != cudaSuccess) { free_stream(c); return cuda_fail(e, "clone"); }
   *out = c;
@@ -1434,6 +1517,17 @@ whff_status_t whff_dstream_get_info(whff_dstream_t s, whff_dstream_info_t* info)
   info->planes_limit = s->planes_limit;
   info->has_raw_flag = s->has_raw;
   info->layout = s->layout;
+  info->packed = s->packed ? 1 : 0;
+  info->device = s->device;
+  info->packed_exceptions = s->pk_nexc;
+  if (s->packed) {
+    const pk::Geom gg = pk::make_geom(s->rows, s->cols);
+    info->packed_bytes = s->pk_body_words * 4 + gg.nband * gg.nsegb * sizeof(pk::Seg) + s->pk_nexc * 72;
+    info->device_bytes += s->pk_alloc_words * 4 + gg.nband * gg.nsegb * sizeof(pk::Seg) +
+                          std::max<uint64_t>(s->pk_nexc, 1) * 72;
+  } else {
+    info->packed_bytes = 0;
+  }
   return WHFF_OK;
 }
 
@@ -1487,6 +1581,7 @@ whff_status_t whff_dstream_rebind(whff_dstream_t s, uint64_t payload_bytes) {
   s->payload_bytes = payload_bytes;
   s->payload_bits = payload_bytes * 8;
   if (s->kind != WHFF_INDEX_IMPLICIT) s->total_bits = s->payload_bits;
+  drop_packed(s);   // new contents: the packed copy is stale (re-pack to use it)
   return WHFF_OK;
 }
 
@@ -1698,6 +1793,7 @@ whff_status_t whff_decode_blocks(whff_dstream_t s, uint64_t first, uint64_t coun
   if (!s) return fail(WHFF_ERR_ARGUMENT, "null stream");
   if (first > s->nb || count > s->nb - first) return fail(WHFF_ERR_CORRUPT, "block index out of range");
   if (count == 0) return WHFF_OK;
+  DeviceGuard g(s->device);
   const int pl = planes_limit < 0 ? s->planes_limit : std::min(planes_limit, kNPlanes);
   const StreamView v = s->view();
   cudaStream_t cs = (cudaStream_t)stream;
@@ -1716,6 +1812,7 @@ whff_status_t whff_decode_block_words(whff_dstream_t s, uint64_t first, uint64_t
   if (!s || !out) return fail(WHFF_ERR_ARGUMENT, "null argument");
   if (first > s->nb || count > s->nb - first) return fail(WHFF_ERR_CORRUPT, "block index out of range");
   if (count == 0) return WHFF_OK;
+  DeviceGuard g(s->device);
   const StreamView v = s->view();
   cudaStream_t cs = (cudaStream_t)stream;
   if (s->has_raw)
@@ -1729,10 +1826,16 @@ whff_status_t whff_decode_block_words(whff_dstream_t s, uint64_t first, uint64_t
 whff_status_t whff_decode(whff_dstream_t s, float* out, uint64_t ld, uint64_t* status,
                           whff_stream_t stream) {
   if (!s || !out || !status) return fail(WHFF_ERR_ARGUMENT, "null argument");
+  DeviceGuard g(s->device);
   if (ld < s->cols) return fail(WHFF_ERR_DIMENSION, "ld_out < cols");
   const StreamView v = s->view();
   cudaStream_t cs = (cudaStream_t)stream;
   auto* st = reinterpret_cast<unsigned long long*>(status);
+  if (s->packed) {
+    cudaError_t e = pk_launch_words(pk_view(s), s->pk_nexc, out, ld, st, cs);
+    if (e != cudaSuccess) return cuda_fail(e, "decode (packed)");
+    return WHFF_OK;
+  }
   const uint64_t warps = s->br * s->gpr;
   if (warps == 0) return WHFF_OK;
   const unsigned grid = (unsigned)((warps + 7) / 8);
@@ -1803,9 +1906,22 @@ static uint64_t ws_rec_bytes(const whff_dstream* s) {
   return align256(std::max<uint64_t>(s->br, 1) * kVW * sizeof(VwRec));
 }
 
+static uint64_t pk_nband(const whff_dstream* s) { return std::max<uint64_t>((s->br + 3) / 4, 1); }
+static uint64_t ws_pkrec_bytes(const whff_dstream* s) { return align256(pk_nband(s) * kPkVW * sizeof(PkRec)); }
+
 extern "C" whff_status_t whff_decode_gemv_workspace_size(whff_dstream_t s, int eval, size_t* bytes) {
   if (!s || !bytes) return fail(WHFF_ERR_ARGUMENT, "null argument");
-  *bytes = ws_u_bytes(s, eval) + ws_rec_bytes(s) + std::max<uint64_t>(s->br, 1) * sizeof(unsigned);
+  if (s->packed)
+    *bytes = ws_u_bytes(s, eval) + ws_pkrec_bytes(s) + pk_nband(s) * sizeof(unsigned);
+  else
+    *bytes = ws_u_bytes(s, eval) + ws_rec_bytes(s) + std::max<uint64_t>(s->br, 1) * sizeof(unsigned);
+  return WHFF_OK;
+}
+
+static whff_status_t launch_pk(int eval, int policy, const PkTable& T, unsigned long long* status,
+                               cudaStream_t cs) {
+  cudaError_t e = pk_launch_gemv(eval, policy, T, status, cs);
+  if (e != cudaSuccess) return cuda_fail(e, "decode_gemv (packed)");
   return WHFF_OK;
 }
 
@@ -1826,7 +1942,37 @@ extern "C" whff_status_t whff_decode_gemv(whff_dstream_t s, const float* v, floa
   if (row_begin > row_end || row_end > s->rows) return fail(WHFF_ERR_DIMENSION, "bad row range");
   if (row_begin == row_end) return WHFF_OK;
   if (!v || !y || !status) return fail(WHFF_ERR_ARGUMENT, "null argument");
+  DeviceGuard g(s->device);
   cudaStream_t cs = (cudaStream_t)stream;
+  if (s->packed) {
+    PkTable T;
+    T.jobs = nullptr;
+    T.prefix = nullptr;
+    T.n = 1;
+    T.single.p = pk_view(s);
+    T.single.v = v;
+    T.single.y = y;
+    T.single.U = nullptr;
+    T.single.row_begin = row_begin;
+    T.single.row_end = row_end;
+    T.single.band0 = row_begin / 16;
+    T.total_bands = (row_end + 15) / 16 - row_begin / 16;
+    size_t need = 0;
+    whff_decode_gemv_workspace_size(s, eval, &need);
+    if (!ws || ws_bytes < need) return fail(WHFF_ERR_ARGUMENT, "workspace too small");
+    if ((reinterpret_cast<uintptr_t>(ws) & 15u) != 0) return fail(WHFF_ERR_ARGUMENT, "workspace alignment");
+    uint8_t* wsb = reinterpret_cast<uint8_t*>(ws);
+    T.recs = reinterpret_cast<PkRec*>(wsb + ws_u_bytes(s, eval));
+    T.tickets = reinterpret_cast<unsigned*>(wsb + ws_u_bytes(s, eval) + ws_pkrec_bytes(s));
+    cudaError_t me = cudaMemsetAsync(T.tickets, 0, T.total_bands * sizeof(unsigned), cs);
+    if (me != cudaSuccess) return cuda_fail(me, "workspace clear");
+    if (eval == WHFF_EVAL_COEFF) {
+      k_coeff_prep<<<grid_for(s->bc, 256), 256, 0, cs>>>(v, s->cols, s->bc, reinterpret_cast<float4*>(ws));
+      WCK_LAUNCH("coeff_prep");
+      T.single.U = reinterpret_cast<const float4*>(ws);
+    }
+    return launch_pk(eval, policy, T, reinterpret_cast<unsigned long long*>(status), cs);
+  }
   JobTable T;
   T.jobs = nullptr;
   T.prefix = nullptr;
@@ -1870,11 +2016,96 @@ struct whff_gemv_plan {
   float4* d_U = nullptr;
   VwRec* d_recs = nullptr;       // [block-row][kVW] partials
   unsigned* d_tickets = nullptr;  // [block-row] arrival counters (reset by the kernel)
+  // packed streams (whff_dstream_pack): band jobs
+  bool pk = false;
+  PkJob* d_pkjobs = nullptr;
+  PkRec* d_pkrecs = nullptr;
   // distinct vectors for the coefficient prologue
   std::vector<const float*> prep_v;
   std::vector<uint64_t> prep_cols, prep_bc, prep_off;
   uint64_t bytes_read = 0, bytes_written = 0, n_blocks = 0;
 };
+
+// distinct vectors of a plan (coefficient prologue) and their U offsets
+static void plan_vectors(whff_gemv_plan* P, int n, const whff_dstream_t* streams, const float* const* v,
+                         std::vector<uint64_t>& uoff, uint64_t& ucount) {
+  uoff.assign(n, 0);
+  ucount = 0;
+  for (int i = 0; i < n; ++i) {
+    const whff_dstream* s = streams[i];
+    int found = -1;
+    for (size_t k = 0; k < P->prep_v.size(); ++k)
+      if (P->prep_v[k] == v[i] && P->prep_cols[k] == s->cols) found = (int)k;
+    if (found < 0) {
+      P->prep_v.push_back(v[i]);
+      P->prep_cols.push_back(s->cols);
+      P->prep_bc.push_back(s->bc);
+      P->prep_off.push_back(ucount);
+      ucount += s->bc;
+      P->bytes_read += s->cols * 4;
+      found = (int)P->prep_v.size() - 1;
+    }
+    uoff[i] = P->prep_off[found];
+  }
+}
+
+static whff_status_t plan_create_packed(int n, const whff_dstream_t* streams, const float* const* v,
+                                        float* const* y, const uint64_t* rb, const uint64_t* re,
+                                        int policy, int eval, whff_gemv_plan_t* out) {
+  for (int i = 0; i < n; ++i)
+    if (rb[i] > re[i] || re[i] > streams[i]->rows) return fail(WHFF_ERR_DIMENSION, "bad row range");
+  whff_gemv_plan* P = new whff_gemv_plan();
+  cudaGetDevice(&P->device);
+  P->n = n;
+  P->policy = policy;
+  P->eval = eval;
+  P->pk = true;
+  std::vector<PkJob> jobs(n);
+  std::vector<uint64_t> prefix(n), uoff;
+  uint64_t bands = 0, ucount = 0;
+  for (int i = 0; i < n; ++i) {
+    const whff_dstream* s = streams[i];
+    PkJob& J = jobs[i];
+    J.p = pk_view(s);
+    J.v = v[i];
+    J.y = y[i];
+    J.U = nullptr;
+    J.row_begin = rb[i];
+    J.row_end = re[i];
+    J.band0 = rb[i] / 16;
+    prefix[i] = bands;
+    const uint64_t b0 = rb[i] / 16, b1 = rb[i] == re[i] ? b0 : (re[i] + 15) / 16;
+    bands += b1 - b0;
+    for (uint64_t b = b0; b < b1; ++b) P->bytes_read += s->pk_band_bytes[b];
+    P->n_blocks += std::min<uint64_t>(b1 * 4, s->br) * s->bc - std::min<uint64_t>(b0 * 4, s->br) * s->bc;
+    P->bytes_written += (re[i] - rb[i]) * 4;
+  }
+  plan_vectors(P, n, streams, v, uoff, ucount);
+  P->total_warps = bands;
+  cudaError_t e = cudaSuccess;
+  if (eval == WHFF_EVAL_COEFF) {
+    e = cudaMalloc(&P->d_U, std::max<uint64_t>(ucount, 1) * sizeof(float4));
+    for (int i = 0; i < n && e == cudaSuccess; ++i) jobs[i].U = P->d_U + uoff[i];
+  }
+  if (e == cudaSuccess) e = cudaMalloc(&P->d_pkjobs, n * sizeof(PkJob));
+  if (e == cudaSuccess) e = cudaMalloc(&P->d_prefix, n * sizeof(uint64_t));
+  if (e == cudaSuccess) e = cudaMemcpy(P->d_pkjobs, jobs.data(), n * sizeof(PkJob), cudaMemcpyHostToDevice);
+  if (e == cudaSuccess) e = cudaMemcpy(P->d_prefix, prefix.data(), n * 8, cudaMemcpyHostToDevice);
+  if (e == cudaSuccess) e = cudaMalloc(&P->d_pkrecs, std::max<uint64_t>(bands, 1) * kPkVW * sizeof(PkRec));
+  if (e == cudaSuccess) e = cudaMalloc(&P->d_tickets, std::max<uint64_t>(bands, 1) * sizeof(unsigned));
+  if (e == cudaSuccess) e = cudaMemset(P->d_tickets, 0, std::max<uint64_t>(bands, 1) * sizeof(unsigned));
+  if (e != cudaSuccess) {
+    cudaFree(P->d_U);
+    cudaFree(P->d_pkjobs);
+    cudaFree(P->d_prefix);
+    cudaFree(P->d_pkrecs);
+    cudaFree(P->d_tickets);
+    delete P;
+    return cuda_fail(e, "plan create (packed)");
+  }
+  *out = P;
+  return WHFF_OK;
+}
 
 extern "C" {
 
@@ -1885,9 +2116,14 @@ whff_status_t whff_gemv_plan_create(int n, const whff_dstream_t* streams, const 
   *out = nullptr;
   whff_status_t st = check_policy_eval(policy, eval);
   if (st != WHFF_OK) return st;
+  for (int i = 0; i < n; ++i)
+    if (!streams[i]) return fail(WHFF_ERR_ARGUMENT, "null stream in plan");
+  bool all_packed = true;
+  for (int i = 0; i < n; ++i) all_packed = all_packed && streams[i]->packed;
+  if (all_packed) return plan_create_packed(n, streams, v, y, rb, re, policy, eval, out);
   const int var = variant_of(streams[0]);
   for (int i = 0; i < n; ++i) {
-    if (!streams[i] || variant_of(streams[i]) != var || streams[i]->mode != streams[0]->mode ||
+    if (variant_of(streams[i]) != var || streams[i]->mode != streams[0]->mode ||
         streams[i]->layout != streams[0]->layout)
       return fail(WHFF_ERR_ARGUMENT, "plan streams must share mode, index kind and layout");
     if (rb[i] > re[i] || re[i] > streams[i]->rows) return fail(WHFF_ERR_DIMENSION, "bad row range");
@@ -1978,6 +2214,7 @@ whff_status_t whff_gemv_plan_create(int n, const whff_dstream_t* streams, const 
 
 whff_status_t whff_gemv_plan_launch(whff_gemv_plan_t P, uint64_t* status, whff_stream_t stream) {
   if (!P || !status) return fail(WHFF_ERR_ARGUMENT, "null argument");
+  DeviceGuard g(P->device);
   cudaStream_t cs = (cudaStream_t)stream;
   if (P->eval == WHFF_EVAL_COEFF) {
     for (size_t k = 0; k < P->prep_v.size(); ++k) {
@@ -1985,6 +2222,17 @@ whff_status_t whff_gemv_plan_launch(whff_gemv_plan_t P, uint64_t* status, whff_s
                                                                  P->prep_bc[k], P->d_U + P->prep_off[k]);
     }
     WCK_LAUNCH("plan coeff_prep");
+  }
+  if (P->pk) {
+    PkTable T;
+    T.jobs = P->d_pkjobs;
+    T.prefix = P->d_prefix;
+    T.n = P->n;
+    T.total_bands = P->total_warps;
+    memset(&T.single, 0, sizeof(T.single));
+    T.recs = P->d_pkrecs;
+    T.tickets = P->d_tickets;
+    return launch_pk(P->eval, P->policy, T, reinterpret_cast<unsigned long long*>(status), cs);
   }
   JobTable T;
   T.jobs = P->d_jobs;
@@ -2015,6 +2263,8 @@ whff_status_t whff_gemv_plan_destroy(whff_gemv_plan_t P) {
   cudaFree(P->d_row_job);
   cudaFree(P->d_recs);
   cudaFree(P->d_tickets);
+  cudaFree(P->d_pkjobs);
+  cudaFree(P->d_pkrecs);
   delete P;
   return WHFF_OK;
 }

@@ -46,7 +46,7 @@ def hostcheck():
     lib = os.path.join(ROOT, "tools", "libhostcheck.so")
     src = os.path.join(ROOT, "tools", "hostcheck.cpp")
     hdrs = [os.path.join(ROOT, "paper_1902_08018_b200", "csrc", h)
-            for h in ("whff_decode.cuh", "whff_encode.cuh", "whff_relayout.cuh")]
+            for h in ("whff_decode.cuh", "whff_encode.cuh", "whff_relayout.cuh", "whff_packed.cuh")]
     if not os.path.exists(lib) or any(os.path.getmtime(p) > os.path.getmtime(lib) for p in hdrs + [src]):
         cxx = "/usr/bin/g++" if os.path.exists("/usr/bin/g++") else "g++"
         subprocess.run([cxx, "-O2", "-std=c++17", "-fPIC", "-shared", "-ffp-contract=off",
@@ -61,6 +61,10 @@ def hostcheck():
     L.hc_encode_blocks.restype = i64
     L.hc_relayout.argtypes = [p, p, p, p, i64, u64, ci, ci, ci]
     L.hc_decode_blocks_sf.argtypes = [p, u64, p, p, i64, ci, ci] + [p] * 6
+    L.hc_pack.argtypes = [p] * 5 + [i64, i64] + [p] * 7
+    L.hc_pack.restype = i64
+    L.hc_unpack.argtypes = [p, p, p, p, i64, i64, i64, p]
+    L.hc_unpack.restype = i64
     return L
 
 

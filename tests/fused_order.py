@@ -217,3 +217,133 @@ def fused_coefficient(orc, stream, v, policy="mixed"):
                     t = fma64(G[i, a], Dt[b, a], t)
                 out[4 * b + i] = np.float32(t)
     return out[:rows]
+
+
+# ---------------------------------------------------------------------------
+# tile-packed layout (k_pk_gemv, csrc/whff_packed.cu)
+# ---------------------------------------------------------------------------
+# * bands of 4 block-rows; a band's segments (256 block-columns) are dealt to
+#   32 virtual warps (segment s -> virtual warp s mod 32); within a segment
+#   tiles t = 0..7 of 32 block-columns, lane l = column 32 (8 s + t) + l;
+# * lane accumulators per (band row i, row r) add, per block, the
+#   coefficient-domain term binary32(w_r * 2^k) (w as fused_coefficient,
+#   every coefficient applied, q exact or rounded for |q| >= 2^24) or the
+#   exact products x[r, j] * v[j] in column order;
+# * exceptions (raw escapes, scales outside 2^-126..2^100) are left out of
+#   the lane sums; per segment, in (tile, row, lane) order, the warp adds
+#   (p0 + p1) + (p2 + p3) of each of their rows to a per-warp sum R;
+# * lane butterfly, virtual-warp butterfly; y = binary32(R + sum_a G D_a) in
+#   the coefficient domain (fma order a = 0..3 onto R), binary32(D + R)
+#   exactly.
+
+def _exceptions(emax, raw):
+    k = emax.astype(np.int64) - EMAX_BIAS - QUANT_BITS
+    return (raw != 0) | ((emax != 0) & ~((k >= -126) & (k <= 100)))
+
+
+def packed_model(orc, stream, v, policy="mixed", evaluation="coefficient"):
+    v = np.asarray(v, np.float32)
+    rows, cols = stream.rows, stream.cols
+    code, _ = orc.mode_kind(stream.mode)
+    payload = np.ascontiguousarray(stream.payload, np.uint8)
+    index = np.ascontiguousarray(stream.block_index, np.uint64)
+    seg = orc.segment_lengths(stream.mode, payload.size, index)
+    mag, neg, emax, raw, raw_words, _ = orc.decode_blocks(
+        payload, index, seg, 27, orc.planes_limit_for(stream.mode), code == 2)
+    words = orc.decompress(stream)
+    bc, br = (cols + 3) // 4, (rows + 3) // 4
+    nband = (br + 3) // 4
+    ntile = (bc + 31) // 32
+    nsegb = (ntile + 7) // 8
+    nbp = nsegb * 256
+    single = policy == "single"
+    acc_t = np.float32 if single else np.float64
+    vp = np.zeros(nbp * 4, np.float32)
+    vp[:cols] = v
+    V = vp.reshape(nbp, 4)
+    exc = np.zeros((nband * 4, nbp), bool)
+    exc[:br, :bc] = _exceptions(emax, raw).reshape(br, bc)
+    Xp = np.zeros((nband * 16, nbp * 4), np.float32)
+    Xp[:rows, :cols] = words
+    X = Xp.reshape(nband * 4, 4, nbp, 4).transpose(0, 2, 1, 3)      # [brow, bcol, r, j]
+    Pf = (X * V[None, :, None, :]).astype(np.float32)
+    if policy == "double":
+        Pf = X.astype(np.float64) * V[None, :, None, :].astype(np.float64)
+    Pa = Pf.astype(acc_t)
+    if evaluation == "coefficient":
+        U = np.zeros((nbp, 4), np.float32)
+        for kk in range(4):
+            t = np.zeros(nbp, np.float64)
+            for j in range(4):
+                t = t + np.float64(G[j, kk]) * V[:, j].astype(np.float64)
+            U[:, kk] = t.astype(np.float32)
+        def pad(a):
+            out = np.zeros((nband * 4, nbp) + a.shape[1:], a.dtype)
+            out[:br, :bc] = a.reshape((br, bc) + a.shape[1:])
+            return out
+        M, N, E = pad(mag), pad(neg), pad(emax)
+        w = np.zeros((nband * 4, nbp, 4), np.float32)
+        for c in range(16):
+            pos = SEQ[c]
+            a, j = pos >> 2, pos & 3
+            q = M[:, :, c].astype(np.float32)            # rounded to binary32 above 2^24
+            q = np.where(N[:, :, c] != 0, -q, q).astype(np.float32)
+            if c == 0:
+                w[:, :, 0] = (q * U[None, :, 0]).astype(np.float32)
+            else:
+                w[:, :, a] = fma32(q, np.broadcast_to(U[None, :, j], q.shape), w[:, :, a])
+        kk = np.clip(E.astype(np.int64) - EMAX_BIAS - QUANT_BITS, -126, 100)
+        sc = np.ldexp(np.float32(1.0), kk).astype(np.float32)
+        use = (E != 0) & ~exc
+        T = np.where(use[:, :, None], (w * sc[:, :, None]).astype(np.float32), np.float32(0))
+        T = T.astype(acc_t)
+    out = np.zeros(nband * 16, np.float32)
+    for band in range(nband):
+        D = np.zeros((32, 32, 4, 4), acc_t)           # [vw, lane, i, r]
+        R = np.zeros((32, 16), acc_t)                 # [vw, 4 i + r]
+        for vw in range(32):
+            for sb in range(vw, nsegb, 32):
+                for tt in range(8):
+                    cs = (8 * sb + tt) * 32 + np.arange(32)
+                    for i in range(4):
+                        b = 4 * band + i
+                        if evaluation == "coefficient":
+                            D[vw, :, i, :] = D[vw, :, i, :] + T[b, cs, :]
+                        else:
+                            m = ~exc[b, cs]
+                            for r in range(4):
+                                for j in range(4):
+                                    D[vw, :, i, r] = np.where(m, D[vw, :, i, r] + Pa[b, cs, r, j],
+                                                              D[vw, :, i, r])
+                for tt in range(8):
+                    for i in range(4):
+                        b = 4 * band + i
+                        for lane in range(32):
+                            col = (8 * sb + tt) * 32 + lane
+                            if col >= bc or b >= br or not exc[b, col]:
+                                continue
+                            for r in range(4):
+                                p = Pa[b, col, r]
+                                R[vw, 4 * i + r] = R[vw, 4 * i + r] + ((p[0] + p[1]) + (p[2] + p[3]))
+        Dv = _butterfly(np.moveaxis(D, 1, -1))         # [vw, i, r]
+        Dt = _butterfly(np.moveaxis(Dv, 0, -1))        # [i, r]
+        Rt = _butterfly(np.moveaxis(R, 0, -1))         # [16]
+        for i in range(4):
+            for r in range(4):
+                if evaluation == "coefficient":
+                    if single:
+                        t = np.float32(Rt[4 * i + r])
+                        for a in range(4):
+                            t = fma32(G[r, a], Dt[i, a], t)[0]
+                        out[16 * band + 4 * i + r] = t
+                    else:
+                        t = float(Rt[4 * i + r])
+                        for a in range(4):
+                            t = fma64(G[r, a], Dt[i, a], t)
+                        out[16 * band + 4 * i + r] = np.float32(t)
+                else:
+                    if single:
+                        out[16 * band + 4 * i + r] = np.float32(Dt[i, r]) + np.float32(Rt[4 * i + r])
+                    else:
+                        out[16 * band + 4 * i + r] = np.float32(float(Dt[i, r]) + float(Rt[4 * i + r]))
+    return out[:rows]

@@ -38,7 +38,7 @@ def test_library_exports_every_declared_symbol():
     for name in declared():
         assert hasattr(L, name), name
     L.whff_abi_version.restype = ctypes.c_int
-    assert L.whff_abi_version() == 1
+    assert L.whff_abi_version() == 2
     L.whff_status_string.restype = ctypes.c_char_p
     L.whff_status_string.argtypes = [ctypes.c_int]
     assert L.whff_status_string(3) == b"corrupt stream"

@@ -212,3 +212,215 @@ void hc_walk_stats(const uint32_t* words, uint64_t payload_bits, const uint64_t*
   }
 }
 }
+
+// ---------------------------------------------------------------------------
+// Tile-packed layout (csrc/whff_packed.cuh): a host packer with the device
+// packer's rules, and an unpacker that reads every fast-path record with
+// the kernels' funnel/magic extraction and checks it against the generic
+// parse.  The GPU tests compare the device packer's output with hc_pack.
+// ---------------------------------------------------------------------------
+#include <algorithm>
+#include <vector>
+
+#include "../paper_1902_08018_b200/csrc/whff_packed.cuh"
+
+namespace {
+struct HostStream {
+  const uint32_t* mag;
+  const uint8_t* neg;
+  const uint16_t* emax;
+  const uint8_t* raw;
+  const uint32_t* raw_words;
+};
+whff::Decoded hs_block(const HostStream& h, uint64_t b) {
+  whff::Decoded d;
+  d.emax = h.emax[b];
+  d.raw = h.raw[b];
+  d.negm = 0;
+  d.consumed = 0;
+  for (int c = 0; c < 16; ++c) {
+    d.mag[c] = d.raw ? h.raw_words[16 * b + c] : h.mag[16 * b + c];
+    if (h.neg[16 * b + c]) d.negm |= 1u << c;
+  }
+  return d;
+}
+}  // namespace
+
+extern "C" {
+
+// Pack (mag, neg, emax, raw, raw_words) of a rows x cols stream.  Pass NULL
+// outputs to size: returns body words; *nseg_out, *nexc_out.
+int64_t hc_pack(const uint32_t* mag, const uint8_t* neg, const uint16_t* emax, const uint8_t* raw,
+                const uint32_t* raw_words, int64_t rows, int64_t cols, uint8_t* segs_out,
+                uint32_t* body_out, uint64_t* exc_block_out, uint32_t* exc_words_out,
+                int64_t* nseg_out, int64_t* nexc_out, int64_t* generic_out) {
+  using namespace whff;
+  const HostStream hs{mag, neg, emax, raw, raw_words};
+  const pk::Geom g = pk::make_geom(rows, cols);
+  const uint64_t nseg = g.nband * g.nsegb;
+  uint64_t body = 0, nexc = 0, generic = 0;
+  for (uint64_t sid = 0; sid < nseg; ++sid) {
+    const uint64_t band = sid / g.nsegb, sb = sid % g.nsegb;
+    const int nrows = pk::band_rows(g, band);
+    const uint64_t col0 = sb * pk::kSegCols, ncols = std::min<uint64_t>(pk::kSegCols, g.bc - col0);
+    int W[16] = {0};
+    uint32_t emin = 0xFFFF, emx = 0, ne = 0;
+    for (int i = 0; i < nrows; ++i)
+      for (uint64_t c = 0; c < ncols; ++c) {
+        const whff::Decoded d = hs_block(hs, (band * 4 + i) * g.bc + col0 + c);
+        if (pk::is_exception(d)) { ++ne; continue; }
+        if (d.emax == 0) continue;
+        emin = std::min(emin, d.emax);
+        emx = std::max(emx, d.emax);
+        int32_t q[16];
+        pk::signed_coefs(d, q);
+        for (int k = 0; k < 16; ++k) W[k] = std::max(W[k], pk::qwidth(q[k]));
+      }
+    if (W[0] < 1) W[0] = 1;
+    const uint32_t ebase = emx >= emin ? emin : 0u;
+    const int We = emx > emin ? pk::bitwidth_u(emx - emin) : 0;
+    pk::Layout f;
+    pk::make_layout(We, W, f);
+    if (!f.fast) ++generic;
+    pk::Seg S;
+    S.body = body;
+    S.hdr = ebase | ((uint32_t)We << 9) | ((f.fast ? 0u : 1u) << 13) | ((f.k2 ? 1u : 0u) << 14) |
+            ((uint32_t)f.L << 16);
+    S.w[0] = S.w[1] = S.w[2] = 0;
+    S.o[0] = S.o[1] = S.o[2] = S.o[3] = 0;
+    for (int c = 0; c < 16; ++c) {
+      S.w[c / 6] |= (uint32_t)W[c] << (5 * (c % 6));
+      if (f.fast) S.o[c / 4] |= (uint32_t)f.o[c] << (8 * (c % 4));
+    }
+    S.exc_begin = (uint32_t)nexc;
+    S.exc_count = ne;
+    const int L = f.L, mf = L >> 5, tb = L & 31;
+    const uint64_t TW = pk::tile_words(nrows, L);
+    const int ntl = pk::seg_tiles(g, sb);
+    if (segs_out) std::memcpy(segs_out + 48 * sid, &S, 48);
+    for (int tt = 0; tt < ntl; ++tt)
+      for (int i = 0; i < nrows; ++i)
+        for (int lane = 0; lane < 32; ++lane) {
+          const uint64_t col = (sb * 8 + tt) * 32 + lane;
+          const uint64_t b = (band * 4 + i) * g.bc + col;
+          int32_t q[16] = {0};
+          uint32_t ed = 0;
+          bool isexc = false;
+          whff::Decoded d;
+          if (col < g.bc) {
+            d = hs_block(hs, b);
+            isexc = pk::is_exception(d);
+            if (!isexc && d.emax != 0) {
+              pk::signed_coefs(d, q);
+              ed = d.emax - ebase;
+            }
+          }
+          uint32_t rec[pk::kMaxRecordWords + 1] = {0};
+          pk::build_record(f, W, ed, q, rec);
+          if (body_out) {
+            const uint64_t rb = body + tt * TW + (uint64_t)i * L;
+            for (int k = 0; k < mf; ++k) body_out[rb + 32 * k + lane] = rec[k];
+            if (tb) {
+              const uint32_t t = rec[mf] & ~(0xFFFFFFFFu >> tb);
+              const uint32_t bit = (uint32_t)lane * tb, sh = bit & 31;
+              uint32_t* tp = body_out + rb + 32 * mf + (bit >> 5);
+              tp[0] |= t >> sh;
+              if (sh) tp[1] |= t << (32 - sh);
+            }
+          }
+          if (isexc) {
+            if (exc_block_out) {
+              exc_block_out[nexc] = b;
+              float x[16];
+              whff::reconstruct_words(d, x);
+              std::memcpy(exc_words_out + 16 * nexc, x, 64);
+            }
+            ++nexc;
+          }
+        }
+    body += ntl * TW;
+  }
+  if (nseg_out) *nseg_out = (int64_t)nseg;
+  if (nexc_out) *nexc_out = (int64_t)nexc;
+  if (generic_out) *generic_out = (int64_t)generic;
+  return (int64_t)body;
+}
+
+// Decode a packed stream to words; fast-path segments are read with the
+// kernels' extraction (fields_int) and checked against parse_record.
+// Returns the number of records where the two disagree.
+int64_t hc_unpack(const uint8_t* segs_in, const uint32_t* body, const uint64_t* exc_block,
+                  const uint32_t* exc_words, int64_t nexc, int64_t rows, int64_t cols, float* out) {
+  using namespace whff;
+  const pk::Geom g = pk::make_geom(rows, cols);
+  int64_t bad = 0;
+  for (uint64_t sid = 0; sid < g.nband * g.nsegb; ++sid) {
+    pk::Seg S;
+    std::memcpy(&S, segs_in + 48 * sid, 48);
+    const uint64_t band = sid / g.nsegb, sb = sid % g.nsegb;
+    const int nrows = pk::band_rows(g, band);
+    int W[16];
+    for (int c = 0; c < 16; ++c) W[c] = pk::seg_W(S, c);
+    pk::Layout f;
+    pk::make_layout(pk::seg_We(S), W, f);
+    const int L = pk::seg_L(S), mf = L >> 5, tb = L & 31;
+    const uint64_t TW = pk::tile_words(nrows, L);
+    pk::FieldPar par[16];
+    for (int c = 0; c < 16; ++c) par[c] = pk::field_param(S, c);
+    for (int tt = 0; tt < pk::seg_tiles(g, sb); ++tt)
+      for (int i = 0; i < nrows; ++i)
+        for (int lane = 0; lane < 32; ++lane) {
+          const uint64_t col = (sb * 8 + tt) * 32 + lane;
+          if (col >= g.bc) continue;
+          const uint32_t* rb = body + S.body + tt * TW + (uint64_t)i * L;
+          uint32_t rec[pk::kMaxRecordWords + 1] = {0};
+          for (int k = 0; k < mf; ++k) rec[k] = rb[32 * k + lane];
+          if (tb) {
+            const uint32_t bit = (uint32_t)lane * tb;
+            const uint32_t* p = rb + 32 * mf + (bit >> 5);
+            rec[mf] = fsl(p[0], p[1], bit & 31) & ~(0xFFFFFFFFu >> tb);
+          }
+          uint32_t ed;
+          int32_t q[16];
+          pk::parse_record(f, W, rec, ed, q);
+          if (!pk::seg_generic(S)) {
+            // the kernels' words: 4 registers, junk below the tail
+            uint32_t a[4] = {0, 0, 0, 0};
+            for (int k = 0; k < 4; ++k) a[k] = k < mf ? rb[32 * k + lane] : 0u;
+            if (mf < 4 && tb) {
+              const uint32_t bit = (uint32_t)lane * tb;
+              const uint32_t* p = rb + 32 * mf + (bit >> 5);
+              a[mf] = fsl(p[0], p[1], bit & 31);
+            }
+            int32_t qf[16];
+            pk::fields_int(a, par, pk::seg_k2(S), qf);
+            const uint32_t ef = pk::field_edelta(a[0], pk::seg_We(S));
+            bool same = ef == ed;
+            for (int c = 0; c < 16; ++c) same = same && qf[c] == q[c];
+            // the magic-float values equal q exactly
+            for (int c = 3; c < 16; ++c) {
+              const int k = pk::field_pair(c, pk::seg_k2(S));
+              same = same && pk::field_f(a[k], a[k + 1], par[c]) == (float)q[c];
+            }
+            if (!same) ++bad;
+          }
+          float x[16];
+          pk::words_from_q(q, (uint32_t)pk::seg_emax_base(S) + ed, x);
+          const uint64_t r0 = (band * 4 + i) * 4, c0 = col * 4;
+          for (int rr = 0; rr < 4; ++rr)
+            for (int j = 0; j < 4; ++j)
+              if ((int64_t)(r0 + rr) < rows && (int64_t)(c0 + j) < cols) out[(r0 + rr) * cols + c0 + j] = x[4 * rr + j];
+        }
+  }
+  for (int64_t e = 0; e < nexc; ++e) {
+    const uint64_t b = exc_block[e];
+    const uint64_t r0 = (b / g.bc) * 4, c0 = (b % g.bc) * 4;
+    for (int k = 0; k < 16; ++k) {
+      const uint64_t r = r0 + (k >> 2), c = c0 + (k & 3);
+      if ((int64_t)r < rows && (int64_t)c < cols) std::memcpy(&out[r * cols + c], &exc_words[16 * e + k], 4);
+    }
+  }
+  return bad;
+}
+
+}  // extern "C"
