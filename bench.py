@@ -65,6 +65,12 @@ def parse():
                          "so the step needs no broadcast and stays CUDA-graph captured; "
                          "broadcast: rank 0 computes S and broadcasts it")
     ap.add_argument("--no-cpu-baseline", action="store_true")
+    ap.add_argument("--variants", default="exact,accuracy:1e-12",
+                    help="extra lines measured after the headline (N=1): 'exact' = the same "
+                         "streams with the reference's products (exact evaluation); "
+                         "'<mode>' = the same step over streams of another codec mode "
+                         "(accuracy:1e-12 is the reference pipeline's default, pipeline.py:50-51); "
+                         "'' = none")
     ap.add_argument("--cpu-sample-cols", type=int, default=8192)
     ap.add_argument("--no-graph", action="store_true")
     ap.add_argument("--latency-steps", type=int, default=1000,
@@ -263,31 +269,46 @@ def _port_task(payload_path):
     return time.perf_counter() - t0, int(d["payload"].size), int(C.size), float(y.sum())
 
 
-def make_cpu_samples(args, tmpdir):
-    """Bounded sample of the workload: one rows x cols chunk of a slit per
-    axis, compressed on the GPU (byte-identical to the reference encoder)."""
+def _sample_task(job):
+    """Compress one sample chunk on the host with the reference's own encoder
+    (oracle/_ref whff.codec.compress; the C port when it is absent) -- no
+    CUDA, no libwhff_b200.so in the reference arm."""
     import numpy as np
-    import torch
-    from paper_1902_08018_b200 import codec, synth
+    from paper_1902_08018_b200 import synth      # host path: numpy only
+    (grid, S, K, rows, cols, kind, param, a, path) = job
+    spec = synth.Spec(grid_rows=grid, grid_cols=grid, S=S, K=K, M=rows, nnz_target=7, seed=7, n_fields=1)
+    # the first `cols` columns of slit 0 of axis a (model.py:258-268, host expression)
+    C = synth.deformation_rows(spec, a, 0.5 + a, 0, rows, ncols=cols)
+    ref = os.path.join(ROOT, "oracle", "_ref")
+    if os.path.isdir(os.path.join(ref, "whff")):
+        sys.path.insert(0, ref)
+        from whff import codec as rc
+        mode = {"rate": rc.FixedRate, "precision": rc.FixedPrecision, "accuracy": rc.FixedAccuracy}[kind](
+            int(param) if kind != "accuracy" else float(param))
+        s = rc.compress(C, mode)
+        payload, index, total_bits = s.payload, s.block_index, s.total_bits
+    else:
+        from oracle import oracle as orc
+        s = orc.compress(C, (kind, int(param) if kind != "accuracy" else float(param)))
+        payload, index, total_bits = s.payload, s.block_index, s.total_bits
+    v = np.random.default_rng(a).random(cols).astype(np.float32)
+    np.savez(path, kind=kind, param=np.array(param), rows=rows, cols=cols,
+             payload=payload, index=index, total_bits=total_bits, v=v)
+    return path
+
+
+def make_cpu_samples(args, tmpdir):
+    """Bounded sample of the workload: the first `--cpu-sample-cols` columns
+    of one slit per axis, compressed on the host by the reference encoder
+    (in a process pool: ~2.5 s per FixedRate(8) chunk)."""
+    import multiprocessing as mp
+    kind, param = args.mode.split(":")
+    param = float(param)
     K = args.slits * args.rows
-    spec = synth.Spec(grid_rows=args.grid, grid_cols=args.grid, S=args.S, K=K, M=args.rows,
-                      nnz_target=7, seed=7, n_fields=1)
-    mode = parse_mode(args.mode)
-    code, param = codec.mode_code(mode)
-    kind = {0: "rate", 1: "precision", 2: "accuracy"}[code]
-    rng = np.random.default_rng(0)
-    paths = []
-    for a in range(3):
-        rows = synth.deformation_rows(spec, a, 0.5 + a, 0, args.rows, device="cuda")
-        rows = rows[:, : args.cpu_sample_cols].contiguous()
-        s = codec.compress(rows, mode)
-        v = rng.random(rows.shape[1]).astype(np.float32)
-        path = os.path.join(tmpdir, f"sample{a}.npz")
-        np.savez(path, kind=kind, param=np.array(param), rows=s.rows, cols=s.cols,
-                 payload=s.payload, index=s.block_index, total_bits=s.total_bits, v=v)
-        paths.append(path)
-    torch.cuda.synchronize()
-    return paths
+    jobs = [(args.grid, args.S, K, args.rows, args.cpu_sample_cols, kind, param, a,
+             os.path.join(tmpdir, f"sample{a}.npz")) for a in range(3)]
+    with mp.get_context("fork").Pool(3) as pool:
+        return pool.map(_sample_task, jobs)
 
 
 def cpu_model():
@@ -325,43 +346,155 @@ def run_cpu_leg(paths, reps, warmup=0):
 # main legs
 # ---------------------------------------------------------------------------
 
+def workload_config(args, world):
+    """The workload both arms report (`config`): what is computed, not how."""
+    if (args.S, args.grid) == (256000, 608):
+        name = "paper-scale WHFF step (configs[2])" if world == 1 else \
+            f"paper-scale WHFF step row-sharded over {world} GPUs (configs[3])"
+    elif args.S == 1024000:
+        name = "4x paper mesh step (configs[4] workload)"
+    else:
+        name = "WHFF step"
+    return {"workload": name + f": thermal T={args.grid}^2 nnz7 + 3 axes x {args.slits} slits x "
+                               f"{args.rows}x{args.S}",
+            "mode": args.mode, "policy": args.policy,
+            "parallelism": f"row-shard{world}" if world > 1 else "single",
+            "l2": "inputs (compressed field) far larger than L2; no flush needed"}
+
+
+def step_stream_bytes(args):
+    """Compressed bytes of the whole step's slit streams at FixedRate (the
+    other modes' sizes depend on the data: None)."""
+    kind, p = args.mode.split(":")
+    if kind != "rate":
+        return None
+    blocks = 3 * args.slits * ((args.rows + 3) // 4) * ((args.S + 3) // 4)
+    return blocks * 16 * int(p) // 8
+
+
 def reference_main(args, world, rank):
+    """The reference's own CPU path (oracle/_ref: whff.codec.decompress +
+    whff.mpgemv.gemv(mixed, sequential), codec.py:296-314, mpgemv.py:54-61) on
+    all host cores, on a bounded sample of this workload; no CUDA context and
+    no repository .so (sample streams come from the reference encoder)."""
     if rank != 0:
         return 0
-    import torch
     tmp = tempfile.mkdtemp()
     paths = make_cpu_samples(args, tmp)
-    # each step = one pass over the 3-axis sample on all cores
     cores = len(os.sched_getaffinity(0)) if hasattr(os, "sched_getaffinity") else os.cpu_count()
-    reps = max(1, (5 * cores) // 6)
+    reps = max(1, (5 * cores) // 6)          # ~2.5 chunks per core per step
     for _ in range(min(args.warmup, 1)):
         run_cpu_leg(paths, 1)
-    times, gbs = [], []
-    total_bytes = 0
-    t_all = 0.0
+    total_bytes, t_all, per_chunk, kind = 0.0, 0.0, [], None
     for _ in range(args.steps):
-        v, wall, cores, kind, per, vals = run_cpu_leg(paths, reps)
-        times.append(wall)
+        v, wall, cores, kind, per, _ = run_cpu_leg(paths, reps)
         t_all += wall
         total_bytes += v * wall * 1e9
+        per_chunk.append(per)
     value = total_bytes / t_all / 1e9
+    full = step_stream_bytes(args)
+    # the full step at this sustained all-core rate (the sample is a labelled
+    # subset of the same workload: ms_per_step is extrapolated linearly)
+    ms_full = 1e3 * full / (value * 1e9) if full else None
+    chunk = f"{args.rows}x{args.cpu_sample_cols}"
     line = {
         "impl": "reference", "metric": METRIC, "value": round(value, 6), "unit": "GB/s",
         "n_gpus": args.gpus, "steps": args.steps, "warmup": args.warmup,
-        "ms_per_step": round(1e3 * t_all / args.steps, 3), "higher_is_better": True,
-        "scaling": "weak", "vs_baseline": None, "dtype": "f32 products, f64 accumulate",
+        "ms_per_step": round(ms_full, 1) if ms_full else round(1e3 * t_all / args.steps, 3),
+        "ms_per_step_kind": ("full step extrapolated linearly from the sample's all-core rate"
+                             if ms_full else "one sample pass"),
+        "sample_ms_per_step": round(1e3 * t_all / args.steps, 3),
+        "higher_is_better": True,
+        "scaling": "strong", "vs_baseline": None, "dtype": "f32 products, f64 accumulate",
         "data": "synthetic (reference smooth-C formula, model.py:252-268)",
-        "config": {"workload": "paper-scale WHFF step sample (configs[2])",
-                   "mode": args.mode, "sample": f"3 axes x {args.rows}x{args.cpu_sample_cols} slit chunk"
-                                                 f" x {reps} per step"},
+        "config": workload_config(args, 1),
         "cpu_baseline": {"value": round(value, 6), "unit": "GB/s", "cores": cores, "kind": kind,
-                         "sample": f"reference codec.decompress + mpgemv.gemv(mixed, sequential), "
-                                   f"{3 * reps} chunks of {args.rows}x{args.cpu_sample_cols} per step"},
+                         "value_1core": round(statistics.mean(
+                             int(__import__("numpy").load(p)["payload"].size) for p in paths)
+                             / statistics.median(per_chunk) / 1e9, 6),
+                         "cpu_model": cpu_model(),
+                         "sample": f"reference codec.decompress + mpgemv.gemv(mixed, sequential) on "
+                                   f"{3 * reps} chunks of {chunk} ({args.mode}; first {args.cpu_sample_cols} "
+                                   f"columns of one slit per axis, streams from the reference encoder) per step"},
         "e2e": {"value": round(value, 6), "unit": "GB/s", "h2d_bytes_per_step": 0,
                 "d2h_bytes_per_step": 0},
+        "gpu_launches": 0,
     }
     print(json.dumps(line), flush=True)
     return 0
+
+
+def measure_variant(fs, steps, warmup, use_graph):
+    """ms per step (graph replays, CUDA events on the current stream) and the
+    fused launch alone, for one more FieldStep over resident streams."""
+    import torch
+    cur = torch.cuda.current_stream()
+    if use_graph:
+        fs.capture()
+    for _ in range(max(3, warmup)):
+        fs.replay()
+    torch.cuda.synchronize()
+    fs.check()
+    e0, e1 = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
+    e0.record(cur)
+    for _ in range(steps):
+        fs.replay()
+    e1.record(cur)
+    torch.cuda.synchronize()
+    fs.check()
+    step_ms = e0.elapsed_time(e1) / steps
+    e0.record(cur)
+    for _ in range(steps):
+        fs.plan.launch(fs.status)
+    e1.record(cur)
+    torch.cuda.synchronize()
+    return step_ms, e0.elapsed_time(e1) / steps
+
+
+def run_variants(args, fs, streams, info, use_graph, hbm):
+    """The driver-visible extra lines: the exact
+    evaluation over the headline's streams and other codec modes."""
+    import copy
+    import torch
+    from paper_1902_08018_b200.executor import FieldStep
+    out = []
+    for spec_ in [s.strip() for s in args.variants.split(",") if s.strip()]:
+        try:
+            if spec_ == "exact":
+                if args.evaluation == "exact":
+                    continue
+                v = FieldStep(fs.A, fs.B, fs.P, streams, args.rows, args.slits, fs.dark, fs.footprint,
+                              fs.dose, policy=args.policy, evaluation="exact")
+                step_ms, kms = measure_variant(v, args.steps, args.warmup, use_graph)
+                vinfo, vmode, veval = info, args.mode, "exact"
+                v.plan.close()
+                del v
+            else:
+                a2 = copy.copy(args)
+                a2.mode = spec_
+                v, _, _, _, vstreams, vinfo = build_field(a2, 1, 0)
+                step_ms, kms = measure_variant(v, args.steps, args.warmup, use_graph)
+                vmode, veval = spec_, args.evaluation
+            kbytes = float(v.plan.bytes_read + v.plan.bytes_written) if spec_ != "exact" else \
+                float(fs.plan.bytes_read + fs.plan.bytes_written)
+            sb = vinfo["stream_bytes_rank"]
+            K = args.slits * args.rows
+            out.append({"mode": vmode, "evaluation": veval, "ms_per_step": round(step_ms, 4),
+                        "value": round(sb / (step_ms / 1e3) / 1e9, 3), "unit": "GB/s",
+                        "gflops": round(3 * K * (2 * args.S - 1) / (step_ms / 1e3) / 1e9, 2),
+                        "stream_bytes": sb, "kernel_ms": round(kms, 4),
+                        "kernel_bytes": int(kbytes),
+                        "frac": round(kbytes / (kms / 1e3) / 1e9 / hbm, 4),
+                        "reference_stream_frac": round(sb / (kms / 1e3) / 1e9 / hbm, 4),
+                        "packed_bits_per_block": vinfo.get("packed_bits_per_block"),
+                        "reference_bits_per_block": vinfo.get("reference_bits_per_block")})
+            if spec_ != "exact":
+                v.plan.close()
+                del v, vstreams
+                torch.cuda.empty_cache()
+        except Exception as exc:   # a variant never hides the headline line
+            out.append({"variant": spec_, "error": f"{type(exc).__name__}: {exc}"})
+    return out
 
 
 def b200_main(args, world, rank, local):
@@ -524,6 +657,7 @@ def b200_main(args, world, rank, local):
 
     pk, pk_kind = peaks()
     hbm = float(pk.get("hbm_gbs", 6650.0))
+    variants = run_variants(args, fs, streams, info, use_graph, hbm) if world == 1 else []
     K = args.slits * args.rows
     flops = 3 * K * (2 * args.S - 1)
     decoded_bytes = 3 * K * args.S * 4
@@ -565,16 +699,10 @@ def b200_main(args, world, rank, local):
                    else "f32 products, f64 accumulate") if args.policy == "mixed" else args.policy),
         "data": "synthetic (reference smooth-C formula model.py:252-268, seed 7); "
                 f"{info['distinct_per_axis']} distinct slits/axis",
-        "config": {"workload": (("paper-scale WHFF step (configs[2])" if (args.S, args.grid) == (256000, 608)
-                                 else "4x paper mesh step (configs[4] workload)" if args.S == 1024000
-                                 else "WHFF step") + f": thermal T={args.grid}^2 nnz7 + "
-                                f"3 axes x {args.slits} slits x {args.rows}x{args.S}"),
-                   "mode": args.mode, "evaluation": args.evaluation, "policy": args.policy,
-                   "layout": args.layout,
-                   "parallelism": f"row-shard{world}" if world > 1 else "single",
-                   "vector_mode": args.vector_mode if world > 1 else None,
-                   "l2": "inputs (compressed field) far larger than L2; no flush needed",
-                   "cuda_graph": use_graph, "index_kind": info["index_kind"]},
+        "config": workload_config(args, world),
+        "impl_config": {"evaluation": args.evaluation, "layout": args.layout,
+                        "vector_mode": args.vector_mode if world > 1 else None,
+                        "cuda_graph": use_graph, "index_kind": info["index_kind"]},
         "gflops": round(flops * args.steps / steps_s / 1e9, 2),
         "decoded_gbs": round(decoded_bytes * args.steps / steps_s / 1e9, 2),
         "per_gpu_gbs": round(value / world, 3),
@@ -597,6 +725,7 @@ def b200_main(args, world, rank, local):
                      "bytes_per_launch": int(kernel_bytes), "kernel_ms": round(kernel_ms, 4),
                      "share_of_step": round(kernel_ms / (total_ms / args.steps), 3),
                      "instruction_roofline": instr},
+        "variants": variants,
         "cpu_baseline": cpu,
         "clocks": clk,
         "setup": info,

@@ -125,13 +125,14 @@ def generate(spec):
     return Operators(spec, A, B, P, phases)
 
 
-def deformation_rows(spec, axis_index, phase, r0, r1, device=None):
+def deformation_rows(spec, axis_index, phase, r0, r1, device=None, ncols=None):
     """Rows [r0, r1) of the smooth C of one axis (model.py:258-268).  On the
-    host this is the reference's expression verbatim; on a CUDA device the
-    same binary64 expression evaluated by torch (float32 result)."""
+    host this is the reference's expression verbatim (optionally only the
+    first `ncols` columns); on a CUDA device the same binary64 expression
+    evaluated by torch (float32 result)."""
     K, S = spec.K, spec.S
     if device is None:
-        j = np.arange(S, dtype=np.float64)
+        j = np.arange(S if ncols is None else min(ncols, S), dtype=np.float64)
         k = np.arange(K, dtype=np.float64)[r0:r1]
         centers = (k / max(K - 1, 1)) * (S - 1)
         width = S * (0.08 + 0.04 * np.sin(2 * np.pi * k / max(K, 1) + axis_index))

@@ -73,6 +73,9 @@ def thermal_step(A64, B, T_k, u_k):
     b, _ = _dev_vec(B)
     _check_vector("T_k", t, n)
     _check_vector("u_k", u, n)
+    if tuple(b.shape) != (n,):
+        # the reference's B.astype(f64) * u fails to broadcast (thermal.py:107)
+        raise DimensionError(f"B has shape {tuple(b.shape)}, expected ({n},)")
     y = csr_matvec(A, t, b, u)
     return y if dev else y.cpu().numpy()
 
@@ -106,10 +109,15 @@ class ThermalState:
     interpolated: object      # (S,) float32 CUDA tensor
 
     @classmethod
-    def initial(cls, T, S):
+    def initial(cls, model, S=None):
+        """thermal.py:25-28: ``initial(model)`` (anything with ``.T`` and
+        ``.S``, the reference's WaferModel included); ``initial(T, S)`` also
+        accepted."""
         torch = _lib.require_cuda()
-        return cls(0, torch.zeros(T, dtype=torch.float32, device="cuda"),
-                   torch.zeros(S, dtype=torch.float32, device="cuda"))
+        T = model if S is not None else model.T
+        S = S if S is not None else model.S
+        return cls(0, torch.zeros(int(T), dtype=torch.float32, device="cuda"),
+                   torch.zeros(int(S), dtype=torch.float32, device="cuda"))
 
 
 class HeatLoad:
@@ -204,16 +212,25 @@ def run_field_thermal(model, field_schedule, load, state, A=None, P=None, B=None
     keys = {(field_schedule.field_id, field_schedule.slit_for_light_step(i, n_slits))
             for i in range(field_schedule.t_l)}
     dev = DeviceHeatLoad(load.dark_load, {k: load.light_load(*k) for k in keys}, load.dose_scale)
-    u = torch.empty_like(state.temperatures)
+    # a reference (numpy) ThermalState: advance a device copy, write back per step
+    host_state = isinstance(state.temperatures, np.ndarray)
+    T_cur = (torch.from_numpy(np.ascontiguousarray(state.temperatures, np.float32)).cuda()
+             if host_state else state.temperatures)
+    u = torch.empty_like(T_cur)
     for i in range(field_schedule.t_l + field_schedule.t_d):
         if i < field_schedule.t_l:
             phase, slit = "light", field_schedule.slit_for_light_step(i, n_slits)
         else:
             phase, slit = "dark", None
         dev.source(field_schedule.field_id, phase, slit, out=u)
-        t_next = csr_matvec(A, state.temperatures, B, u)
+        t_next = csr_matvec(A, T_cur, B, u)
         s_next = csr_matvec(P, t_next)
+        T_cur = t_next
         state.k += 1
-        state.temperatures = t_next
-        state.interpolated = s_next
+        if host_state:
+            state.temperatures = t_next.cpu().numpy()
+            state.interpolated = s_next.cpu().numpy()
+        else:
+            state.temperatures = t_next
+            state.interpolated = s_next
         yield state.k, phase, slit, (s_next if phase == "light" else None)
