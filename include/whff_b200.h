@@ -154,6 +154,12 @@ whff_status_t whff_dstream_packed_download(whff_dstream_t s, uint8_t* segs_host,
 /* Physically distinct device copy of a stream (same device).  Synchronous. */
 whff_status_t whff_dstream_clone(whff_dstream_t s, whff_dstream_t* out);
 whff_status_t whff_dstream_get_info(whff_dstream_t s, whff_dstream_info_t* info);
+/* Start bit of every block-row in the WHFZ payload, out_host[0..br] (br =
+ * ceil(rows/4); out_host[br] = payload bits).  Block-rows are contiguous in
+ * the stream (codec.py:157-164), so out[b+1] - out[b] is the compressed size
+ * of block-row b: the weight of the byte-balanced row sharding
+ * (executor.shard_units).  Synchronous.                         */
+whff_status_t whff_dstream_block_row_bits(whff_dstream_t s, uint64_t* out_host);
 /* Copy payload (payload_bytes) and u64 block bit offsets (n_blocks) back to
  * the host, e.g. for codec.py:388-402 save_stream.  Synchronous.           */
 /* Streaming scan staging (pipeline.py:208-289 stage 1, the paper's transfer

@@ -17,4 +17,7 @@ chmod -R u+w "$TMP/pkg"
 rm -rf "$HERE/_ref"
 python -m pip install --quiet --no-index --no-build-isolation --no-deps \
   --find-links /opt/wheelhouse --target "$HERE/_ref" "$TMP/pkg"
+# the reference's own test-suite travels with the build (git-ignored): the
+# drop-in test runs it against the B200 plugin (tests/test_gpu_dropin.py)
+cp -r "$TMP/pkg/tests" "$HERE/_ref/_reference_tests"
 PYTHONPATH="$HERE/_ref" python -c "import whff; assert whff.BACKEND_NAME == 'compiled', whff.BACKEND_NAME; print('oracle/_ref: whff', whff.__version__, whff.BACKEND_NAME)"

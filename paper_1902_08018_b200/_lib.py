@@ -54,6 +54,7 @@ _SIG = {
     "whff_dstream_pack": ([_P, _P], _I),
     "whff_dstream_packed_download": ([_P, _P, _P, _P, _P, _P, _P, _P], _I),
     "whff_dstream_get_info": ([_P, _P], _I),
+    "whff_dstream_block_row_bits": ([_P, _P], _I),
     "whff_dstream_download": ([_P, _P, _P], _I),
     "whff_dstream_export": ([_P, _P, _P, _P, _P], _I),
     "whff_dstream_reserve": ([_P, _U64], _I),

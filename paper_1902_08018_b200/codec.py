@@ -221,6 +221,13 @@ class DeviceStream:
         self._refresh()
         return self
 
+    def block_row_bytes(self):
+        """Compressed bytes of every block-row (whff_dstream_block_row_bits):
+        the weights of the byte-balanced row sharding (executor.shard_units)."""
+        out = np.zeros(self.block_rows + 1, dtype=np.uint64)
+        _lib.call("whff_dstream_block_row_bits", self._h, _lib.ptr(out))
+        return (np.diff(out.astype(np.int64)) + 7) // 8
+
     def clone(self):
         """A physically distinct HBM copy (whff_dstream_clone)."""
         h = ctypes.c_void_p()

@@ -1531,6 +1531,22 @@ whff_status_t whff_dstream_get_info(whff_dstream_t s, whff_dstream_info_t* info)
   return WHFF_OK;
 }
 
+whff_status_t whff_dstream_block_row_bits(whff_dstream_t s, uint64_t* out) {
+  if (!s || !out) return fail(WHFF_ERR_ARGUMENT, "null argument");
+  DeviceGuard g(s->device);
+  out[s->br] = s->payload_bits;
+  if (s->kind == WHFF_INDEX_IMPLICIT) {
+    for (uint64_t b = 0; b < s->br; ++b) out[b] = std::min<uint64_t>(b * s->bc * s->seg_bits, s->payload_bits);
+    return WHFF_OK;
+  }
+  // compact: base[b * gpr] is block (b, 0); full: starts[b * bc]
+  const uint64_t* src = s->kind == WHFF_INDEX_COMPACT ? s->d_base : s->d_starts;
+  const uint64_t pitch = (s->kind == WHFF_INDEX_COMPACT ? s->gpr : s->bc) * sizeof(uint64_t);
+  cudaError_t e = cudaMemcpy2D(out, sizeof(uint64_t), src, pitch, sizeof(uint64_t), s->br, cudaMemcpyDeviceToHost);
+  if (e != cudaSuccess) return cuda_fail(e, "block_row_bits");
+  return WHFF_OK;
+}
+
 // index arrays of a stream as one blob: compact = base (br*gpr u64) + lens
 // (nb u16); full = starts (nb u64) + lens (nb u16); implicit = nothing
 static uint64_t index_blob_bytes(const whff_dstream* s) {
@@ -1950,6 +1966,7 @@ extern "C" whff_status_t whff_decode_gemv(whff_dstream_t s, const float* v, floa
     T.prefix = nullptr;
     T.n = 1;
     T.single.p = pk_view(s);
+    T.max_nsegb = T.single.p.g.nsegb;
     T.single.v = v;
     T.single.y = y;
     T.single.U = nullptr;
@@ -2018,6 +2035,7 @@ struct whff_gemv_plan {
   unsigned* d_tickets = nullptr;  // [block-row] arrival counters (reset by the kernel)
   // packed streams (whff_dstream_pack): band jobs
   bool pk = false;
+  uint64_t pk_max_nsegb = 0;      // widest band (segments) of any job
   PkJob* d_pkjobs = nullptr;
   PkRec* d_pkrecs = nullptr;
   // distinct vectors for the coefficient prologue
@@ -2067,6 +2085,7 @@ static whff_status_t plan_create_packed(int n, const whff_dstream_t* streams, co
     const whff_dstream* s = streams[i];
     PkJob& J = jobs[i];
     J.p = pk_view(s);
+    P->pk_max_nsegb = std::max<uint64_t>(P->pk_max_nsegb, J.p.g.nsegb);
     J.v = v[i];
     J.y = y[i];
     J.U = nullptr;
@@ -2229,6 +2248,7 @@ whff_status_t whff_gemv_plan_launch(whff_gemv_plan_t P, uint64_t* status, whff_s
     T.prefix = P->d_prefix;
     T.n = P->n;
     T.total_bands = P->total_warps;
+    T.max_nsegb = P->pk_max_nsegb;
     memset(&T.single, 0, sizeof(T.single));
     T.recs = P->d_pkrecs;
     T.tickets = P->d_tickets;

@@ -41,6 +41,7 @@ struct PkTable {
   const uint64_t* prefix;    // first band of each job
   int n;
   uint64_t total_bands;
+  uint64_t max_nsegb;        // widest band of any job, in segments (kernel choice)
   PkJob single;
   PkRec* recs;               // [band][kVW]
   unsigned* tickets;         // [band] (zero between launches)

@@ -10,7 +10,8 @@ issued as ONE persistent fused decode+GEMV launch over every (slit, block-row)
 job (whff_gemv_plan_*).
 
 Sharding (multi-GPU): the (axis, slit, block-row) units of the field are
-split into N contiguous, equal-count ranges; rank r decodes only its range
+split into N contiguous ranges of equal count (FixedRate: equal bytes) or of
+equal compressed bytes (variable-rate modes, `weights`); rank r decodes only its range
 (its streams are the only ones it holds), so the step needs no data-path
 collective except the tiny S broadcast (or a replicated thermal step) and the
 all-gather of the per-rank deformation rows.  The rows never split a
@@ -71,8 +72,31 @@ class Unit:
     brow: int
 
 
-def shard_units(n_axes, n_slits, rows_per_slit, world, rank):
-    """Contiguous equal split of the (axis, slit, block-row) units.
+def unit_bounds(n_units, world, weights=None):
+    """Contiguous split of n_units ordered units over `world` ranks:
+    boundaries b[0] = 0 <= b[1] <= ... <= b[world] = n_units.  Equal counts
+    without weights; with per-unit weights (compressed bytes of each block-
+    row: variable-rate modes are balanced by bytes) rank r starts
+    at the first unit whose preceding weight reaches r/world of the total."""
+    if weights is None:
+        return [n_units * r // world for r in range(world + 1)]
+    w = np.asarray(weights, dtype=np.int64).reshape(-1)
+    if w.size != n_units or (w < 0).any():
+        raise ValueError("weights: one nonnegative value per unit")
+    excl = np.concatenate([[0], np.cumsum(w)[:-1]]) if n_units else np.zeros(0, np.int64)
+    total = int(w.sum())
+    b = [0]
+    for r in range(1, world):
+        # first u whose preceding weight reaches floor(total * r / world)
+        b.append(int(np.searchsorted(excl, (total * r) // world, side="left")))
+    b.append(n_units)
+    return [max(b[i], b[i - 1]) if i else b[i] for i in range(len(b))]
+
+
+def shard_units(n_axes, n_slits, rows_per_slit, world, rank, weights=None):
+    """Contiguous split of the (axis, slit, block-row) units: equal counts,
+    or balanced by `weights` (one per unit, in unit order, e.g. the
+    compressed bytes of each block-row from DeviceStream.block_row_bytes).
 
     Returns, for this rank, a list of (axis, slit, row_begin, row_end) jobs and
     the global unit range.  Concatenating every rank's rows in rank order
@@ -80,8 +104,8 @@ def shard_units(n_axes, n_slits, rows_per_slit, world, rank):
     """
     bpr = (rows_per_slit + 3) // 4
     total = n_axes * n_slits * bpr
-    u0 = total * rank // world
-    u1 = total * (rank + 1) // world
+    bounds = unit_bounds(total, world, weights)
+    u0, u1 = bounds[rank], bounds[rank + 1]
     jobs = []
     u = u0
     while u < u1:
@@ -95,16 +119,23 @@ def shard_units(n_axes, n_slits, rows_per_slit, world, rank):
     return jobs, (u0, u1)
 
 
-def shard_row_counts(n_axes, n_slits, rows_per_slit, world):
+def shard_row_counts(n_axes, n_slits, rows_per_slit, world, weights=None):
     """Rows owned by each rank, per axis (for un-padding the all-gather)."""
     out = []
     for r in range(world):
-        jobs, _ = shard_units(n_axes, n_slits, rows_per_slit, world, r)
+        jobs, _ = shard_units(n_axes, n_slits, rows_per_slit, world, r, weights)
         counts = [0] * n_axes
         for axis, _, r0, r1 in jobs:
             counts[axis] += r1 - r0
         out.append(counts)
     return out
+
+
+def unit_weights(streams, n_axes, n_slits):
+    """Per-unit compressed bytes (axis, slit, block-row order) from device
+    streams (every streams[axis][slit] must be present)."""
+    return np.concatenate([streams[a][s].block_row_bytes() for a in range(n_axes)
+                           for s in range(n_slits)])
 
 
 class FieldStep:
@@ -116,7 +147,7 @@ class FieldStep:
 
     def __init__(self, A, B, P, streams, rows_per_slit, n_slits, dark, footprint, dose=1.0,
                  policy="mixed", evaluation="exact", world=1, rank=0, group=None,
-                 vector_mode="broadcast"):
+                 vector_mode="broadcast", weights=None):
         torch = _lib.require_cuda()
         self.A, self.B, self.P = A, B, P
         self.dark, self.footprint, self.dose = dark, footprint, dose
@@ -131,10 +162,10 @@ class FieldStep:
         self.u = torch.zeros(T, dtype=torch.float32, device=dev)
         self.S = torch.zeros(S, dtype=torch.float32, device=dev)
         self.status = _lib.status_word(dev)
-        jobs, self.unit_range = shard_units(self.n_axes, n_slits, rows_per_slit, world, rank)
+        jobs, self.unit_range = shard_units(self.n_axes, n_slits, rows_per_slit, world, rank, weights)
         self.jobs = jobs
         self.local_rows = sum(r1 - r0 for _, _, r0, r1 in jobs)
-        counts = shard_row_counts(self.n_axes, n_slits, rows_per_slit, world)
+        counts = shard_row_counts(self.n_axes, n_slits, rows_per_slit, world, weights)
         self.rank_rows = [sum(c) for c in counts]
         self.max_rows = max(self.rank_rows)
         self.local = torch.zeros(self.max_rows, dtype=torch.float32, device=dev)
@@ -169,14 +200,23 @@ class FieldStep:
             dist.broadcast(self.S, src=0, group=self.group)
         self.products()
 
+    _list_gather = False
+
     def gather(self):
-        """All-gather the per-rank deformation rows (padded to max_rows)."""
+        """All-gather the per-rank deformation rows (padded to max_rows): one
+        all_gather_into_tensor on every backend that has it (NCCL; gloo
+        where it supports the tensor's device), the list form otherwise."""
         import torch.distributed as dist
-        if dist.get_backend(self.group) == "nccl":
-            dist.all_gather_into_tensor(self.gathered, self.local, group=self.group)
-        else:  # gloo (CPU tests, several ranks on one device): list form
-            parts = list(self.gathered.view(self.world, self.max_rows).unbind(0))
-            dist.all_gather(parts, self.local, group=self.group)
+        if not self._list_gather:
+            try:
+                dist.all_gather_into_tensor(self.gathered, self.local, group=self.group)
+                return
+            except (RuntimeError, NotImplementedError, ValueError):
+                if dist.get_backend(self.group) == "nccl":
+                    raise
+                self._list_gather = True
+        parts = list(self.gathered.view(self.world, self.max_rows).unbind(0))
+        dist.all_gather(parts, self.local, group=self.group)
 
     def step(self):
         self.step_local()

@@ -301,13 +301,24 @@ def packed_model(orc, stream, v, policy="mixed", evaluation="coefficient"):
     for band in range(nband):
         D = np.zeros((32, 32, 4, 4), acc_t)           # [vw, lane, i, r]
         R = np.zeros((32, 16), acc_t)                 # [vw, 4 i + r]
+        kahan = evaluation == "coefficient" and not single
+        if kahan:   # k_pk_gemv2: compensated binary32 pairs (s, c), s + c in binary64 at the end
+            Ks = np.zeros((32, 32, 4, 4), np.float32)
+            Kc = np.zeros((32, 32, 4, 4), np.float32)
         for vw in range(32):
             for sb in range(vw, nsegb, 32):
                 for tt in range(8):
                     cs = (8 * sb + tt) * 32 + np.arange(32)
                     for i in range(4):
                         b = 4 * band + i
-                        if evaluation == "coefficient":
+                        if kahan:
+                            t = T[b, cs, :].astype(np.float32)
+                            s0 = Ks[vw, :, i, :]
+                            s1 = (s0 + t).astype(np.float32)
+                            d = (s0 - s1).astype(np.float32)
+                            Kc[vw, :, i, :] = (Kc[vw, :, i, :] + (d + t).astype(np.float32)).astype(np.float32)
+                            Ks[vw, :, i, :] = s1
+                        elif evaluation == "coefficient":
                             D[vw, :, i, :] = D[vw, :, i, :] + T[b, cs, :]
                         else:
                             m = ~exc[b, cs]
@@ -325,6 +336,8 @@ def packed_model(orc, stream, v, policy="mixed", evaluation="coefficient"):
                             for r in range(4):
                                 p = Pa[b, col, r]
                                 R[vw, 4 * i + r] = R[vw, 4 * i + r] + ((p[0] + p[1]) + (p[2] + p[3]))
+        if kahan:
+            D = Ks.astype(np.float64) + Kc.astype(np.float64)
         Dv = _butterfly(np.moveaxis(D, 1, -1))         # [vw, i, r]
         Dt = _butterfly(np.moveaxis(Dv, 0, -1))        # [i, r]
         Rt = _butterfly(np.moveaxis(R, 0, -1))         # [16]

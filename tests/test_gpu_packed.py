@@ -232,3 +232,17 @@ def test_packed_rebind_drops_copy(rng):
     assert ds.packed
     ds.rebind(ds.payload_bytes)
     assert not ds.packed
+
+
+@pytest.mark.parametrize("policy", ["mixed", "single"])
+def test_staged_kernel_wide_bands(orc, policy, rng):
+    """More than 32 segments per virtual warp (cols > 1,048,576: the staged
+    kernel's header ring wraps) and row ranges: bit-exact vs the CPU model."""
+    from fused_order import packed_model
+    from paper_1902_08018_b200 import codec
+    C0 = smooth_matrix(9, 1_100_003, S=1_100_003)
+    s = codec.compress(C0, codec.FixedRate(8))
+    v = rng.random(C0.shape[1]).astype(np.float32)
+    got = _packed_gemv(s, v, policy, "coefficient")
+    want = packed_model(orc, s, v, policy, "coefficient")
+    assert np.array_equal(got.view(np.uint32), want.view(np.uint32))

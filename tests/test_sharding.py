@@ -73,3 +73,27 @@ def test_gloo_two_rank_gather_reassembles_field():
         p.join(timeout=60)
     want = list(range(3 * 5 * 13))
     assert res[0] == want and res[1] == want
+
+
+@pytest.mark.parametrize("world", [1, 2, 3, 8])
+def test_byte_balanced_shards(world):
+    """Variable-rate modes split by compressed bytes: contiguous,
+    covering, and every rank within one unit's weight of total / world."""
+    from paper_1902_08018_b200.executor import unit_bounds
+    rng = np.random.default_rng(world)
+    n_axes, n_slits, rows = 3, 7, 30
+    bpr = (rows + 3) // 4
+    w = rng.integers(20, 400, n_axes * n_slits * bpr)
+    w[5:40] *= 9                                   # a heavy region
+    b = unit_bounds(w.size, world, w)
+    assert b[0] == 0 and b[-1] == w.size and all(x <= y for x, y in zip(b, b[1:]))
+    loads = [int(w[b[r]:b[r + 1]].sum()) for r in range(world)]
+    assert max(loads) - w.sum() / world <= w.max()
+    seen = []
+    for r in range(world):
+        jobs, (u0, u1) = shard_units(n_axes, n_slits, rows, world, r, w)
+        assert (u0, u1) == (b[r], b[r + 1])
+        for axis, slit, r0, r1 in jobs:
+            seen.extend((axis, slit, i) for i in range(r0, r1))
+    assert seen == [(a, s, i) for a in range(n_axes) for s in range(n_slits) for i in range(rows)]
+    assert unit_bounds(10, 3, np.ones(10)) == unit_bounds(10, 3)
