@@ -67,8 +67,7 @@ __global__ void __launch_bounds__(256) k_pk_stats(StreamView s, pk::Geom g, pk::
   pk::make_layout(We, W, f);
   pk::Seg S;
   S.body = 0;
-  S.hdr = ebase | ((uint32_t)We << 9) | ((f.fast ? 0u : 1u) << 13) | ((f.k2 ? 1u : 0u) << 14) |
-          ((uint32_t)f.L << 16);
+  S.hdr = pk::seg_hdr(ebase, f);
   S.w[0] = S.w[1] = S.w[2] = 0;
   S.o[0] = S.o[1] = S.o[2] = S.o[3] = 0;
   for (int c = 0; c < 16; ++c) {
@@ -78,7 +77,7 @@ __global__ void __launch_bounds__(256) k_pk_stats(StreamView s, pk::Geom g, pk::
   S.exc_begin = 0;
   S.exc_count = nexc;
   segs[sid] = S;
-  seg_words[sid] = (uint64_t)pk::seg_tiles(g, sb) * pk::tile_words(nrows, f.L);
+  seg_words[sid] = (uint64_t)pk::seg_tiles(g, sb) * pk::tile_words(f.L);
   seg_exc[sid] = nexc;
 }
 
@@ -112,9 +111,9 @@ __global__ void __launch_bounds__(256) k_pk_emit(StreamView s, pk::Geom g, const
   int W[16];
   pk::Layout f;
   seg_layout(S, W, f);
-  const int L = f.L, mf = L >> 5, tb = L & 31;
+  const int L = f.L, R = pk::rec_words(L);
   const uint32_t ebase = (uint32_t)pk::seg_emax_base(S);
-  const uint64_t TW = pk::tile_words(nrows, L);
+  const uint64_t TW = pk::tile_words(L);
   uint64_t exc = S.exc_begin;
   const int ntl = pk::seg_tiles(g, sb);
   for (int tt = 0; tt < ntl; ++tt) {
@@ -146,20 +145,9 @@ __global__ void __launch_bounds__(256) k_pk_emit(StreamView s, pk::Geom g, const
       }
       // zero blocks, exceptions and absent lanes: q = 0 (offset-binary 2^(W-1))
       pk::build_record(f, W, ed, q, rec);
-      // record group of (tile tt, row i)
-      const uint64_t rb = S.body + tt * TW + (uint64_t)i * L;
-      for (int k = 0; k < mf; ++k) body[rb + 32 * k + lane] = rec[k];
-      if (tb) {
-        // tail: record bits [32 mf, L) at tail bits [lane tb, lane tb + tb)
-        const uint32_t t = rec[mf] & ~(0xFFFFFFFFu >> tb);     // top tb bits
-        const uint32_t bit = (uint32_t)lane * tb;
-        uint32_t* tp = body + rb + 32 * mf + (bit >> 5);
-        const uint32_t sh = bit & 31;
-        if (t) {
-          atomicOr(tp, t >> sh);
-          if (sh && (t << (32 - sh))) atomicOr(tp + 1, t << (32 - sh));
-        }
-      }
+      // word-major tile: word k of (row i, lane) at tile word (32 k + lane) * 4 + i
+      uint32_t* tp = body + S.body + tt * TW;
+      for (int k = 0; k < R; ++k) tp[pk::tile_word(k, lane, i)] = rec[k];
       // exceptions in (tile, row, lane) order
       const unsigned m = __ballot_sync(0xFFFFFFFFu, isexc);
       if (isexc) {

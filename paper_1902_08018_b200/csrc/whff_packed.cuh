@@ -22,19 +22,20 @@
 //              fields at offsets fixed per segment; field 0 (DC) is two's
 //              complement, fields 1..15 offset-binary (q + 2^(W-1)).
 //
-// Records are MSB-first bit strings of L bits (L per segment).  The 32
-// records of one block-row of a tile form a "record group" of exactly L
-// words: the first floor(L/32) words of each record interleaved across the
-// lanes (word k of lane l at 32 k + l: one coalesced 128-byte load per k),
-// then the 32 tails of L mod 32 bits packed back to back.  A tile is
-// nrows record groups padded to 16 bytes; a segment body is its tiles.
+// Records are MSB-first bit strings of L bits (L per segment), stored in
+// R = ceil(L / 32) whole 32-bit words.  A tile holds the records of its 4
+// block-rows x 32 block-columns word-major: word k of the record of (row i,
+// lane l) is tile word (32 k + l) * 4 + i, so one 16-byte shared-memory
+// load by lane l yields word k of all four rows (rows past the band's end
+// are zero records).  A tile is 128 R words; a segment body is its tiles.
 //
-// Fast path (every segment of a smooth WHFF operator, L <= 128): field c is
-// read from a static register pair (a_k, a_k+1) of the record's four words,
-// k = 0 for c <= 1, 0 or 1 for c = 2 (segment flag), 1 for c = 3..8 and 2
-// for c = 9..15 (the packer pads so each field lies inside its pair), with
-// two funnel shifts: the left one brings the field to the top, the right one
-// shifts it down under the binary32 exponent of 2^23 ("magic number"), so
+// Fast path (every segment of a smooth WHFF operator, L <= 160): field c is
+// read from a register pair (a_k, a_k+1) of the record's five words chosen
+// per segment from two candidates: k = 0 for c <= 1, 0 or 1 for c = 2
+// (flag k2), 1 or 2 for c = 3..8 (flag kA), 2 or 3 for c = 9..15 (flag kB)
+// (the packer pads so each field lies inside its pair), with two funnel
+// shifts: the left one brings the field to the top, the right one shifts it
+// down under the binary32 exponent of 2^23 ("magic number"), so
 // float(2^23 + u) - (2^23 + 2^(W-1)) = q exactly (W <= 23).  Segments whose
 // fields do not fit (adversarial data) take a generic per-lane path.
 //
@@ -58,14 +59,15 @@ constexpr int kSegCols = kTile * kSegTiles;
 constexpr int kMagicW = 23;       // widest offset-binary field on the magic path
 constexpr int kMaxRecordBits = 9 + 28 * 16;
 constexpr int kMaxRecordWords = (kMaxRecordBits + 31) / 32;   // 15
+constexpr int kFastWords = 5;                                 // fast path: L <= 160
 constexpr uint32_t kMagic = 0x4B000000u;                      // binary32 2^23
 
 // Segment header (48 bytes).
 struct alignas(16) Seg {
   uint64_t body;       // word offset of the segment body
-  uint32_t hdr;        // [0:9) emax_base [9:13) W_e [13] generic [14] k2 [16:25) L
+  uint32_t hdr;        // [0:9) emax_base [9:13) W_e [13] generic [14] k2 [15] kA [16:25) L [25] kB
   uint32_t w[3];       // W_c, 5 bits each: c = 6 * word + slot
-  uint32_t o[4];       // fast path: offset of field c (7 bits): c = 4 * word + slot
+  uint32_t o[4];       // fast path: offset of field c (8 bits): c = 4 * word + slot
   uint32_t exc_begin;  // first exception of the segment
   uint32_t exc_count;
 };
@@ -74,46 +76,64 @@ WHFF_HD int seg_emax_base(const Seg& s) { return (int)(s.hdr & 511u); }
 WHFF_HD int seg_We(const Seg& s) { return (int)((s.hdr >> 9) & 15u); }
 WHFF_HD bool seg_generic(const Seg& s) { return (s.hdr >> 13) & 1u; }
 WHFF_HD bool seg_k2(const Seg& s) { return (s.hdr >> 14) & 1u; }
+WHFF_HD bool seg_kA(const Seg& s) { return (s.hdr >> 15) & 1u; }
+WHFF_HD bool seg_kB(const Seg& s) { return (s.hdr >> 25) & 1u; }
 WHFF_HD int seg_L(const Seg& s) { return (int)((s.hdr >> 16) & 511u); }
 WHFF_HD int seg_W(const Seg& s, int c) { return (int)((s.w[c / 6] >> (5 * (c % 6))) & 31u); }
-WHFF_HD int seg_o(const Seg& s, int c) { return (int)((s.o[c / 4] >> (8 * (c % 4))) & 127u); }
+WHFF_HD int seg_o(const Seg& s, int c) { return (int)((s.o[c / 4] >> (8 * (c % 4))) & 255u); }
 
-// static register pair of field c on the fast path (c = 2: the segment flag)
-WHFF_HD int field_pair(int c, bool k2) { return c <= 1 ? 0 : c == 2 ? (k2 ? 1 : 0) : c <= 8 ? 1 : 2; }
+// register pair of field c on the fast path (the segment's flags)
+WHFF_HD int field_pair(int c, bool k2, bool kA, bool kB) {
+  return c <= 1 ? 0 : c == 2 ? (k2 ? 1 : 0) : c <= 8 ? (kA ? 2 : 1) : (kB ? 3 : 2);
+}
 
 // Field offsets from the widths (W[0] >= 1).  Fast layout: fields in order,
-// each inside the 64-bit window of its static register pair (bits
-// [32k, 32k + 64) of the record; padded up to 32k when needed); generic
-// (fields back to back) when a field does not fit or a field c >= 1 is
-// wider than the magic path allows.
+// each inside the 64-bit window of its register pair (bits [32k, 32k + 64)
+// of the record; padded up to 32k when needed), a group (c = 2, 3..8,
+// 9..15) taking its second candidate pair only when the first cannot hold
+// it; generic (fields back to back) when a field does not fit, a field
+// c >= 3 is wider than the magic path allows, or L > 160.
 struct Layout {
   int We, L;
-  bool fast, k2;
+  bool fast, k2, kA, kB;
   int o[16];
 };
+WHFF_HD bool place_group(const int W[16], int c0, int c1, int k, int& cur, int o[16]) {
+  int x = cur < 32 * k ? 32 * k : cur;
+  for (int c = c0; c <= c1; ++c) {
+    if (W[c] == 0) { o[c] = 0; continue; }
+    if (x + W[c] > 32 * k + 64) return false;
+    o[c] = x;
+    x += W[c];
+  }
+  cur = x;
+  return true;
+}
 WHFF_HD void make_layout(int We, const int W[16], Layout& f) {
   int cur = We;
-  bool fast = true, k2 = false;
-  for (int c = 0; c < 16; ++c) {
-    f.o[c] = 0;
-    if (W[c] == 0) continue;
-    int k;
-    if (c <= 1) {
-      k = 0;
-    } else if (c == 2) {
-      k = cur + W[c] <= 64 ? 0 : 1;
-      k2 = k == 1;
-    } else {
-      k = c <= 8 ? 1 : 2;
-    }
-    if (c >= 3 && W[c] > kMagicW) fast = false;   // (c = 1, 2 convert as integers)
-    if (cur < 32 * k) cur = 32 * k;
-    if (cur + W[c] > 32 * k + 64) fast = false;
-    f.o[c] = cur;
-    cur += W[c];
+  bool fast = true;
+  f.k2 = f.kA = f.kB = false;
+  for (int c = 0; c < 16; ++c) f.o[c] = 0;
+  for (int c = 3; c < 16; ++c)
+    if (W[c] > kMagicW) fast = false;   // (c = 1, 2 convert as integers)
+  if (fast) fast = place_group(W, 0, 1, 0, cur, f.o);
+  if (fast) {
+    int t = cur, o2[16];
+    if (place_group(W, 2, 2, 0, t, o2)) { f.o[2] = o2[2]; cur = t; }
+    else { f.k2 = true; fast = place_group(W, 2, 2, 1, cur, f.o); }
+  }
+  if (fast) {
+    int t = cur, oA[16];
+    if (place_group(W, 3, 8, 1, t, oA)) { for (int c = 3; c <= 8; ++c) f.o[c] = oA[c]; cur = t; }
+    else { f.kA = true; fast = place_group(W, 3, 8, 2, cur, f.o); }
+  }
+  if (fast) {
+    int t = cur, oB[16];
+    if (place_group(W, 9, 15, 2, t, oB)) { for (int c = 9; c <= 15; ++c) f.o[c] = oB[c]; cur = t; }
+    else { f.kB = true; fast = place_group(W, 9, 15, 3, cur, f.o); }
   }
   if (!fast) {
-    k2 = false;
+    f.k2 = f.kA = f.kB = false;
     cur = We;
     for (int c = 0; c < 16; ++c) {
       f.o[c] = cur;
@@ -123,7 +143,12 @@ WHFF_HD void make_layout(int We, const int W[16], Layout& f) {
   f.We = We;
   f.L = cur;
   f.fast = fast;
-  f.k2 = k2;
+}
+
+// segment header word from a layout
+WHFF_HD uint32_t seg_hdr(uint32_t ebase, const Layout& f) {
+  return ebase | ((uint32_t)f.We << 9) | ((f.fast ? 0u : 1u) << 13) | ((f.k2 ? 1u : 0u) << 14) |
+         ((f.kA ? 1u : 0u) << 15) | ((uint32_t)f.L << 16) | ((f.kB ? 1u : 0u) << 25);
 }
 
 // signed width: the fewest bits holding q in two's complement / offset binary
@@ -134,8 +159,11 @@ WHFF_HD int qwidth(int32_t q) {
 }
 WHFF_HD int bitwidth_u(uint32_t x) { return x == 0 ? 0 : 32 - (int)clz32(x); }
 
-// words of one tile: nrows record groups of L words, padded to 16 bytes
-WHFF_HD uint64_t tile_words(int nrows, int L) { return ((uint64_t)nrows * L + 3) & ~3ull; }
+// words of one record / tile (4 row slots x 32 lanes)
+WHFF_HD int rec_words(int L) { return (L + 31) >> 5; }
+WHFF_HD uint64_t tile_words(int L) { return 128ull * (uint64_t)rec_words(L); }
+// tile word holding word k of the record of (row i, lane l)
+WHFF_HD uint32_t tile_word(int k, int lane, int i) { return ((uint32_t)(32 * k + lane) << 2) | (uint32_t)i; }
 
 // Geometry of a packed stream.
 struct Geom {
@@ -261,7 +289,7 @@ WHFF_HD FieldPar field_param(const Seg& S, int c) {
     p.z = 32u;
     p.w = c <= 2 ? 0u : 0xCB000000u;         // -2^23
   } else {
-    const int k = field_pair(c, seg_k2(S));
+    const int k = field_pair(c, seg_k2(S), seg_kA(S), seg_kB(S));
     p.x = (uint32_t)(seg_o(S, c) - 32 * k);
     p.y = c <= 2 ? 0u : kMagic >> W;
     p.z = 32u - (uint32_t)W;
@@ -299,12 +327,13 @@ WHFF_HD uint32_t field_edelta(uint32_t a0, int We) { return fsr(a0, 0u, 32u - (u
 
 // All 16 coefficients (sequency order) of one fast-path record a[0..3]
 // (the host check's form; the kernels read par from shared memory).
-WHFF_HD void fields_int(const uint32_t a[4], const FieldPar par[16], bool k2, int32_t q[16]) {
+WHFF_HD void fields_int(const uint32_t a[kFastWords], const FieldPar par[16], bool k2, bool kA, bool kB,
+                        int32_t q[16]) {
   q[0] = field_dc(a[0], a[1], par[0]);
-  q[1] = field_i(a[0], a[1], par[1]);
-  q[2] = k2 ? field_i(a[1], a[2], par[2]) : field_i(a[0], a[1], par[2]);
-  for (int c = 3; c <= 8; ++c) q[c] = field_i(a[1], a[2], par[c]);
-  for (int c = 9; c < 16; ++c) q[c] = field_i(a[2], a[3], par[c]);
+  for (int c = 1; c < 16; ++c) {
+    const int k = field_pair(c, k2, kA, kB);
+    q[c] = field_i(a[k], k + 1 < kFastWords ? a[k + 1] : 0u, par[c]);
+  }
 }
 }  // namespace pk
 }  // namespace whff

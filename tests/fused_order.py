@@ -301,31 +301,34 @@ def packed_model(orc, stream, v, policy="mixed", evaluation="coefficient"):
     for band in range(nband):
         D = np.zeros((32, 32, 4, 4), acc_t)           # [vw, lane, i, r]
         R = np.zeros((32, 16), acc_t)                 # [vw, 4 i + r]
-        kahan = evaluation == "coefficient" and not single
-        if kahan:   # k_pk_gemv2: compensated binary32 pairs (s, c), s + c in binary64 at the end
-            Ks = np.zeros((32, 32, 4, 4), np.float32)
-            Kc = np.zeros((32, 32, 4, 4), np.float32)
+        staged = evaluation == "coefficient"     # k_pk_gemv2's order
+        if staged:
+            # per segment: per-lane binary32 sums over the segment's tiles (one
+            # FMA-rounding per term), then the warp's transpose reduction over
+            # the 32 lanes (the xor-16..1 butterfly) in binary64 (single:
+            # binary32), accumulated per segment in the virtual warp's order
+            Dv_acc = np.zeros((32, 16), acc_t)
         for vw in range(32):
             for sb in range(vw, nsegb, 32):
+                if staged:
+                    Sg = np.zeros((32, 4, 4), np.float32)          # [lane, i, r]
                 for tt in range(8):
                     cs = (8 * sb + tt) * 32 + np.arange(32)
                     for i in range(4):
                         b = 4 * band + i
-                        if kahan:
-                            t = T[b, cs, :].astype(np.float32)
-                            s0 = Ks[vw, :, i, :]
-                            s1 = (s0 + t).astype(np.float32)
-                            d = (s0 - s1).astype(np.float32)
-                            Kc[vw, :, i, :] = (Kc[vw, :, i, :] + (d + t).astype(np.float32)).astype(np.float32)
-                            Ks[vw, :, i, :] = s1
+                        if staged:
+                            Sg[:, i, :] = (Sg[:, i, :] + T[b, cs, :].astype(np.float32)).astype(np.float32)
                         elif evaluation == "coefficient":
-                            D[vw, :, i, :] = D[vw, :, i, :] + T[b, cs, :]
+                            raise AssertionError("unreachable")
                         else:
                             m = ~exc[b, cs]
                             for r in range(4):
                                 for j in range(4):
                                     D[vw, :, i, r] = np.where(m, D[vw, :, i, r] + Pa[b, cs, r, j],
                                                               D[vw, :, i, r])
+                if staged:
+                    Dseg = Sg.reshape(32, 16).astype(acc_t)          # [lane, m = 4 i + r]
+                    Dv_acc[vw] = Dv_acc[vw] + _butterfly(np.moveaxis(Dseg, 0, -1))
                 for tt in range(8):
                     for i in range(4):
                         b = 4 * band + i
@@ -336,9 +339,10 @@ def packed_model(orc, stream, v, policy="mixed", evaluation="coefficient"):
                             for r in range(4):
                                 p = Pa[b, col, r]
                                 R[vw, 4 * i + r] = R[vw, 4 * i + r] + ((p[0] + p[1]) + (p[2] + p[3]))
-        if kahan:
-            D = Ks.astype(np.float64) + Kc.astype(np.float64)
-        Dv = _butterfly(np.moveaxis(D, 1, -1))         # [vw, i, r]
+        if staged:
+            Dv = Dv_acc.reshape(32, 4, 4)
+        else:
+            Dv = _butterfly(np.moveaxis(D, 1, -1))     # [vw, i, r]
         Dt = _butterfly(np.moveaxis(Dv, 0, -1))        # [i, r]
         Rt = _butterfly(np.moveaxis(R, 0, -1))         # [16]
         for i in range(4):

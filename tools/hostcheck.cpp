@@ -284,8 +284,7 @@ int64_t hc_pack(const uint32_t* mag, const uint8_t* neg, const uint16_t* emax, c
     if (!f.fast) ++generic;
     pk::Seg S;
     S.body = body;
-    S.hdr = ebase | ((uint32_t)We << 9) | ((f.fast ? 0u : 1u) << 13) | ((f.k2 ? 1u : 0u) << 14) |
-            ((uint32_t)f.L << 16);
+    S.hdr = pk::seg_hdr(ebase, f);
     S.w[0] = S.w[1] = S.w[2] = 0;
     S.o[0] = S.o[1] = S.o[2] = S.o[3] = 0;
     for (int c = 0; c < 16; ++c) {
@@ -294,8 +293,8 @@ int64_t hc_pack(const uint32_t* mag, const uint8_t* neg, const uint16_t* emax, c
     }
     S.exc_begin = (uint32_t)nexc;
     S.exc_count = ne;
-    const int L = f.L, mf = L >> 5, tb = L & 31;
-    const uint64_t TW = pk::tile_words(nrows, L);
+    const int L = f.L, R = pk::rec_words(L);
+    const uint64_t TW = pk::tile_words(L);
     const int ntl = pk::seg_tiles(g, sb);
     if (segs_out) std::memcpy(segs_out + 48 * sid, &S, 48);
     for (int tt = 0; tt < ntl; ++tt)
@@ -318,15 +317,8 @@ int64_t hc_pack(const uint32_t* mag, const uint8_t* neg, const uint16_t* emax, c
           uint32_t rec[pk::kMaxRecordWords + 1] = {0};
           pk::build_record(f, W, ed, q, rec);
           if (body_out) {
-            const uint64_t rb = body + tt * TW + (uint64_t)i * L;
-            for (int k = 0; k < mf; ++k) body_out[rb + 32 * k + lane] = rec[k];
-            if (tb) {
-              const uint32_t t = rec[mf] & ~(0xFFFFFFFFu >> tb);
-              const uint32_t bit = (uint32_t)lane * tb, sh = bit & 31;
-              uint32_t* tp = body_out + rb + 32 * mf + (bit >> 5);
-              tp[0] |= t >> sh;
-              if (sh) tp[1] |= t << (32 - sh);
-            }
+            uint32_t* tp = body_out + body + tt * TW;
+            for (int k = 0; k < R; ++k) tp[pk::tile_word(k, lane, i)] = rec[k];
           }
           if (isexc) {
             if (exc_block_out) {
@@ -363,8 +355,8 @@ int64_t hc_unpack(const uint8_t* segs_in, const uint32_t* body, const uint64_t* 
     for (int c = 0; c < 16; ++c) W[c] = pk::seg_W(S, c);
     pk::Layout f;
     pk::make_layout(pk::seg_We(S), W, f);
-    const int L = pk::seg_L(S), mf = L >> 5, tb = L & 31;
-    const uint64_t TW = pk::tile_words(nrows, L);
+    const int L = pk::seg_L(S), R = pk::rec_words(L);
+    const uint64_t TW = pk::tile_words(L);
     pk::FieldPar par[16];
     for (int c = 0; c < 16; ++c) par[c] = pk::field_param(S, c);
     for (int tt = 0; tt < pk::seg_tiles(g, sb); ++tt)
@@ -372,35 +364,25 @@ int64_t hc_unpack(const uint8_t* segs_in, const uint32_t* body, const uint64_t* 
         for (int lane = 0; lane < 32; ++lane) {
           const uint64_t col = (sb * 8 + tt) * 32 + lane;
           if (col >= g.bc) continue;
-          const uint32_t* rb = body + S.body + tt * TW + (uint64_t)i * L;
+          const uint32_t* tp = body + S.body + tt * TW;
           uint32_t rec[pk::kMaxRecordWords + 1] = {0};
-          for (int k = 0; k < mf; ++k) rec[k] = rb[32 * k + lane];
-          if (tb) {
-            const uint32_t bit = (uint32_t)lane * tb;
-            const uint32_t* p = rb + 32 * mf + (bit >> 5);
-            rec[mf] = fsl(p[0], p[1], bit & 31) & ~(0xFFFFFFFFu >> tb);
-          }
+          for (int k = 0; k < R; ++k) rec[k] = tp[pk::tile_word(k, lane, i)];
           uint32_t ed;
           int32_t q[16];
           pk::parse_record(f, W, rec, ed, q);
           if (!pk::seg_generic(S)) {
-            // the kernels' words: 4 registers, junk below the tail
-            uint32_t a[4] = {0, 0, 0, 0};
-            for (int k = 0; k < 4; ++k) a[k] = k < mf ? rb[32 * k + lane] : 0u;
-            if (mf < 4 && tb) {
-              const uint32_t bit = (uint32_t)lane * tb;
-              const uint32_t* p = rb + 32 * mf + (bit >> 5);
-              a[mf] = fsl(p[0], p[1], bit & 31);
-            }
+            // the kernels' words: five registers (words past the record are 0)
+            uint32_t a[pk::kFastWords] = {0, 0, 0, 0, 0};
+            for (int k = 0; k < pk::kFastWords && k < R; ++k) a[k] = rec[k];
             int32_t qf[16];
-            pk::fields_int(a, par, pk::seg_k2(S), qf);
+            pk::fields_int(a, par, pk::seg_k2(S), pk::seg_kA(S), pk::seg_kB(S), qf);
             const uint32_t ef = pk::field_edelta(a[0], pk::seg_We(S));
             bool same = ef == ed;
             for (int c = 0; c < 16; ++c) same = same && qf[c] == q[c];
             // the magic-float values equal q exactly
             for (int c = 3; c < 16; ++c) {
-              const int k = pk::field_pair(c, pk::seg_k2(S));
-              same = same && pk::field_f(a[k], a[k + 1], par[c]) == (float)q[c];
+              const int k = pk::field_pair(c, pk::seg_k2(S), pk::seg_kA(S), pk::seg_kB(S));
+              same = same && pk::field_f(a[k], k + 1 < pk::kFastWords ? a[k + 1] : 0u, par[c]) == (float)q[c];
             }
             if (!same) ++bad;
           }
