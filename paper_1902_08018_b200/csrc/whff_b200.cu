@@ -736,9 +736,15 @@ __global__ void WHFF_GEMV_LB k_decode_gemv(JobTable T, unsigned long long* statu
 }
 
 // u_b = G^T v_b per block-column (coefficient-domain prologue)
-__global__ void k_coeff_prep(const float* v, uint64_t cols, uint64_t bc, float4* U) {
+// U = G^T v per block-column, zero-padded to whole 32-column tiles (bcp)
+static uint64_t pad_tiles(uint64_t bc) { return (bc + 31) & ~31ull; }
+__global__ void k_coeff_prep(const float* v, uint64_t cols, uint64_t bc, uint64_t bcp, float4* U) {
   const uint64_t b = blockIdx.x * (uint64_t)blockDim.x + threadIdx.x;
-  if (b >= bc) return;
+  if (b >= bcp) return;
+  if (b >= bc) {
+    U[b] = make_float4(0.f, 0.f, 0.f, 0.f);
+    return;
+  }
   const float4 x = load_v4(v, b, cols, false);
   const float xv[4] = {x.x, x.y, x.z, x.w};
   float u[4];
@@ -1155,11 +1161,12 @@ void drop_packed(whff_dstream* s) {
 
 PkView pk_view(const whff_dstream* s) {
   PkView v;
+  v.g = pk::make_geom(s->rows, s->cols);
   v.body = s->d_pk_body;
   v.segs = s->d_pk_segs;
+  v.pars = s->d_pk_segs ? reinterpret_cast<const pk::FieldPar*>(s->d_pk_segs + v.g.nband * v.g.nsegb) : nullptr;
   v.exc_block = s->d_pk_exc_block;
   v.exc_words = s->d_pk_exc_words;
-  v.g = pk::make_geom(s->rows, s->cols);
   return v;
 }
 
@@ -1365,7 +1372,7 @@ whff_status_t whff_dstream_pack(whff_dstream_t s, whff_stream_t stream) {
   uint64_t *words = nullptr, *exc = nullptr, *off = nullptr, *eoff = nullptr;
   void* tmp = nullptr;
   size_t tmp_bytes = 0, t2 = 0;
-  cudaError_t e = cudaMalloc(&segs, nseg * sizeof(pk::Seg));
+  cudaError_t e = cudaMalloc(&segs, pk_segs_bytes(nseg));
   if (e == cudaSuccess) e = cudaMalloc(&words, (nseg + 1) * 8);
   if (e == cudaSuccess) e = cudaMalloc(&exc, (nseg + 1) * 8);
   if (e == cudaSuccess) e = cudaMalloc(&off, (nseg + 1) * 8);
@@ -1393,6 +1400,7 @@ whff_status_t whff_dstream_pack(whff_dstream_t s, whff_stream_t stream) {
   if (e == cudaSuccess) e = cudaMemcpyAsync(&tot[1], eoff + nseg, 8, cudaMemcpyDeviceToHost, cs);
   if (e == cudaSuccess) e = cudaStreamSynchronize(cs);
   if (e == cudaSuccess) e = pk_launch_finalize(segs, nseg, off, eoff, cs);
+  if (e == cudaSuccess) e = pk_launch_params(segs, nseg, cs);
   // readable slack past the body: rows past a band's end and tails read ahead
   const uint64_t alloc_words = tot[0] + 4 * pk::kMaxRecordWords * 32 + 64;
   uint32_t* body = nullptr;
@@ -1426,7 +1434,8 @@ whff_status_t whff_dstream_pack(whff_dstream_t s, whff_stream_t stream) {
   s->pk_band_bytes.assign(gg.nband, 0);
   for (uint64_t b = 0; b < gg.nband; ++b) {
     const uint64_t s0 = b * gg.nsegb, s1 = s0 + gg.nsegb;
-    s->pk_band_bytes[b] = (hoff[s1] - hoff[s0]) * 4 + gg.nsegb * sizeof(pk::Seg) + (hexc[s1] - hexc[s0]) * 72;
+    s->pk_band_bytes[b] = (hoff[s1] - hoff[s0]) * 4 + gg.nsegb * (sizeof(pk::Seg) + 16 * sizeof(pk::FieldPar)) +
+                          (hexc[s1] - hexc[s0]) * 72;
   }
   s->packed = true;
   return WHFF_OK;
@@ -1483,9 +1492,9 @@ whff_status_t whff_dstream_clone(whff_dstream_t s, whff_dstream_t* out) {
     e = cudaMalloc(&c->d_pk_body, s->pk_alloc_words * 4);
     if (e == cudaSuccess)
       e = cudaMemcpy(c->d_pk_body, s->d_pk_body, s->pk_alloc_words * 4, cudaMemcpyDeviceToDevice);
-    if (e == cudaSuccess) e = cudaMalloc(&c->d_pk_segs, nseg * sizeof(pk::Seg));
+    if (e == cudaSuccess) e = cudaMalloc(&c->d_pk_segs, pk_segs_bytes(nseg));
     if (e == cudaSuccess)
-      e = cudaMemcpy(c->d_pk_segs, s->d_pk_segs, nseg * sizeof(pk::Seg), cudaMemcpyDeviceToDevice);
+      e = cudaMemcpy(c->d_pk_segs, s->d_pk_segs, pk_segs_bytes(nseg), cudaMemcpyDeviceToDevice);
     const uint64_t ne = std::max<uint64_t>(s->pk_nexc, 1);
     if (e == cudaSuccess) e = cudaMalloc(&c->d_pk_exc_block, ne * 8);
     if (e == cudaSuccess) e = cudaMemcpy(c->d_pk_exc_block, s->d_pk_exc_block, ne * 8, cudaMemcpyDeviceToDevice);
@@ -1522,8 +1531,8 @@ whff_status_t whff_dstream_get_info(whff_dstream_t s, whff_dstream_info_t* info)
   info->packed_exceptions = s->pk_nexc;
   if (s->packed) {
     const pk::Geom gg = pk::make_geom(s->rows, s->cols);
-    info->packed_bytes = s->pk_body_words * 4 + gg.nband * gg.nsegb * sizeof(pk::Seg) + s->pk_nexc * 72;
-    info->device_bytes += s->pk_alloc_words * 4 + gg.nband * gg.nsegb * sizeof(pk::Seg) +
+    info->packed_bytes = s->pk_body_words * 4 + pk_segs_bytes(gg.nband * gg.nsegb) + s->pk_nexc * 72;
+    info->device_bytes += s->pk_alloc_words * 4 + pk_segs_bytes(gg.nband * gg.nsegb) +
                           std::max<uint64_t>(s->pk_nexc, 1) * 72;
   } else {
     info->packed_bytes = 0;
@@ -1916,7 +1925,7 @@ static whff_status_t launch_gemv(int var, int eval, bool sf, const JobTable& T, 
 // [per-row virtual-warp partials][per-row arrival counters]
 static uint64_t align256(uint64_t x) { return (x + 255) & ~255ull; }
 static uint64_t ws_u_bytes(const whff_dstream* s, int eval) {
-  return eval == WHFF_EVAL_COEFF ? align256(s->bc * sizeof(float4)) : 0;
+  return eval == WHFF_EVAL_COEFF ? align256(pad_tiles(s->bc) * sizeof(float4)) : 0;
 }
 static uint64_t ws_rec_bytes(const whff_dstream* s) {
   return align256(std::max<uint64_t>(s->br, 1) * kVW * sizeof(VwRec));
@@ -1984,7 +1993,8 @@ extern "C" whff_status_t whff_decode_gemv(whff_dstream_t s, const float* v, floa
     cudaError_t me = cudaMemsetAsync(T.tickets, 0, T.total_bands * sizeof(unsigned), cs);
     if (me != cudaSuccess) return cuda_fail(me, "workspace clear");
     if (eval == WHFF_EVAL_COEFF) {
-      k_coeff_prep<<<grid_for(s->bc, 256), 256, 0, cs>>>(v, s->cols, s->bc, reinterpret_cast<float4*>(ws));
+      k_coeff_prep<<<grid_for(pad_tiles(s->bc), 256), 256, 0, cs>>>(v, s->cols, s->bc, pad_tiles(s->bc),
+                                                                 reinterpret_cast<float4*>(ws));
       WCK_LAUNCH("coeff_prep");
       T.single.U = reinterpret_cast<const float4*>(ws);
     }
@@ -2013,7 +2023,8 @@ extern "C" whff_status_t whff_decode_gemv(whff_dstream_t s, const float* v, floa
   cudaError_t me = cudaMemsetAsync(T.tickets, 0, T.total_warps * sizeof(unsigned), cs);
   if (me != cudaSuccess) return cuda_fail(me, "workspace clear");
   if (eval == WHFF_EVAL_COEFF) {
-    k_coeff_prep<<<grid_for(s->bc, 256), 256, 0, cs>>>(v, s->cols, s->bc, reinterpret_cast<float4*>(ws));
+    k_coeff_prep<<<grid_for(pad_tiles(s->bc), 256), 256, 0, cs>>>(v, s->cols, s->bc, pad_tiles(s->bc),
+                                                               reinterpret_cast<float4*>(ws));
     WCK_LAUNCH("coeff_prep");
     T.single.U = reinterpret_cast<const float4*>(ws);
   }
@@ -2059,7 +2070,7 @@ static void plan_vectors(whff_gemv_plan* P, int n, const whff_dstream_t* streams
       P->prep_cols.push_back(s->cols);
       P->prep_bc.push_back(s->bc);
       P->prep_off.push_back(ucount);
-      ucount += s->bc;
+      ucount += pad_tiles(s->bc);
       P->bytes_read += s->cols * 4;
       found = (int)P->prep_v.size() - 1;
     }
@@ -2188,7 +2199,7 @@ whff_status_t whff_gemv_plan_create(int n, const whff_dstream_t* streams, const 
       P->prep_cols.push_back(s->cols);
       P->prep_bc.push_back(s->bc);
       P->prep_off.push_back(ucount);
-      ucount += s->bc;
+      ucount += pad_tiles(s->bc);
       P->bytes_read += s->cols * 4;
       found = (int)P->prep_v.size() - 1;
     }
@@ -2237,8 +2248,8 @@ whff_status_t whff_gemv_plan_launch(whff_gemv_plan_t P, uint64_t* status, whff_s
   cudaStream_t cs = (cudaStream_t)stream;
   if (P->eval == WHFF_EVAL_COEFF) {
     for (size_t k = 0; k < P->prep_v.size(); ++k) {
-      k_coeff_prep<<<grid_for(P->prep_bc[k], 256), 256, 0, cs>>>(P->prep_v[k], P->prep_cols[k],
-                                                                 P->prep_bc[k], P->d_U + P->prep_off[k]);
+      k_coeff_prep<<<grid_for(pad_tiles(P->prep_bc[k]), 256), 256, 0, cs>>>(
+          P->prep_v[k], P->prep_cols[k], P->prep_bc[k], pad_tiles(P->prep_bc[k]), P->d_U + P->prep_off[k]);
     }
     WCK_LAUNCH("plan coeff_prep");
   }

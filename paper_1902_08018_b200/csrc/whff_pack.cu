@@ -163,6 +163,19 @@ __global__ void __launch_bounds__(256) k_pk_emit(StreamView s, pk::Geom g, const
   }
 }
 
+// per-segment parameter tables (after the headers): one thread per (segment, field)
+__global__ void k_pk_params(const pk::Seg* segs, uint64_t nseg, pk::FieldPar* pars) {
+  const uint64_t t = blockIdx.x * (uint64_t)blockDim.x + threadIdx.x;
+  if (t >= nseg * 16) return;
+  const pk::Seg S = segs[t >> 4];
+  pars[t] = pk::seg_generic(S) ? pk::FieldPar{0u, 0u, 0u, 0u} : pk::seg_param(S, (int)(t & 15));
+}
+
+cudaError_t pk_launch_params(pk::Seg* segs, uint64_t nseg, cudaStream_t cs) {
+  if (nseg) k_pk_params<<<grid_of(nseg * 16, 256), 256, 0, cs>>>(segs, nseg, reinterpret_cast<pk::FieldPar*>(segs + nseg));
+  return cudaGetLastError();
+}
+
 cudaError_t pk_launch_stats(const StreamView& s, const pk::Geom& g, pk::Seg* segs, uint64_t* seg_words,
                             uint64_t* seg_exc, cudaStream_t cs) {
   const uint64_t nseg = g.nband * g.nsegb;

@@ -9,6 +9,15 @@
 #include "whff_packed.cuh"
 #include "whff_packed_api.h"
 
+// f(std::integral_constant<int, c>) for c = C0..C1, fully unrolled
+template <int C0, int C1, class F>
+__device__ __forceinline__ void unroll_range(F&& f) {
+  if constexpr (C0 <= C1) {
+    f(std::integral_constant<int, C0>());
+    unroll_range<C0 + 1, C1>(f);
+  }
+}
+
 // field widths / layout of a segment header
 __device__ __forceinline__ void seg_layout(const pk::Seg& S, int W[16], pk::Layout& f) {
 #pragma unroll
@@ -332,15 +341,21 @@ __global__ void __launch_bounds__(32 * kPkWarps, 2) k_pk_exact(PkTable T, unsign
 // Same virtual-warp decomposition as k_pk_exact (4 warps per CTA, 8 CTAs per
 // band).  Built for the B200's issue rate:
 //   * every warp runs its own kP2Stages-deep ring of shared-memory stages;
-//     lane 0 fills it with 1-D bulk copies (cp.async.bulk, the TMA engine)
-//     of whole tiles (4 block-rows x 32 block-columns of records, word-major,
-//     contiguous in HBM) plus the tile's slice of U = G^T v, completing on a
-//     per-stage mbarrier: no registers hold loads in flight and the copies
-//     of the next tiles overlap the decode of this one;
+//     lane 0 fills each stage with two 1-D bulk copies (cp.async.bulk, the
+//     TMA engine): up to kP2ItemTiles consecutive tiles of a segment (4
+//     block-rows x 32 block-columns of records each, word-major, contiguous
+//     in HBM) and their slice of U = G^T v, completing on the stage's
+//     mbarrier: no registers hold loads in flight and the copies of the next
+//     items overlap the decode of this one;
 //   * one 16-byte shared load per record word gives that word of all four
 //     block-rows; the rows are decoded as two pairs with the packed-f32x2
-//     pipe (FADD2 for the magic-number conversion, FFMA2 for coefficient x u
-//     and for the 2^k-scaled accumulation);
+//     pipe (FFMA2/FADD2 for the exact conversions, FFMA2 for coefficient x u
+//     and for the 2^k-scaled accumulation); the small fields of a group (c =
+//     3..8, 9..15) come out of one 64-bit shift per row and one LOP3 each;
+//   * the per-segment field parameters are precomputed by the packer and
+//     prefetched one segment ahead; the tile body is compiled for the two
+//     layouts almost every smooth segment has (all groups present, or DC and
+//     the two large AC coefficients only) besides the general one;
 //   * per segment (8 tiles) each lane sums its 2^k (Q u) terms per (block-
 //     row, row) in binary32; at the segment's end the warp reduces the 16
 //     sums over its 32 lanes in binary64 with a transpose reduction (8 + 4 +
@@ -349,16 +364,21 @@ __global__ void __launch_bounds__(32 * kPkWarps, 2) k_pk_exact(PkTable T, unsign
 // Generic segments (fields too wide for the fast path) and exceptions take
 // per-lane paths on global memory.
 #ifndef WHFF_P2_STAGES
-#define WHFF_P2_STAGES 4
+#define WHFF_P2_STAGES 2
 #endif
 #ifndef WHFF_P2_MINB
 #define WHFF_P2_MINB 4
 #endif
+#ifndef WHFF_P2_ITEM
+#define WHFF_P2_ITEM 2
+#endif
 constexpr int kP2Warps = 4;                              // warps per CTA
 constexpr int kP2Split = kPkVW / kP2Warps;               // CTAs per band
 constexpr int kP2Stages = WHFF_P2_STAGES;
+constexpr int kP2ItemTiles = WHFF_P2_ITEM;               // tiles per stage
 constexpr int kP2TileBytes = 128 * pk::kFastWords * 4;   // fast path: <= 5 record words
-constexpr int kP2StageBytes = kP2TileBytes + 32 * 16;    // + the U slice
+constexpr int kP2UBytes = kP2ItemTiles * 32 * 16;        // the items' slice of U
+constexpr int kP2StageBytes = kP2ItemTiles * kP2TileBytes + kP2UBytes;
 constexpr int kP2HdrRing = 32;                           // segment headers held per warp
 constexpr int kP2HdrChunk = 16;
 
@@ -376,6 +396,11 @@ __device__ __forceinline__ uint32_t smem_addr(const void* p) {
 }
 __device__ __forceinline__ void mbar_init(uint64_t* bar, unsigned count) {
   asm volatile("mbarrier.init.shared::cta.b64 [%0], %1;" ::"r"(smem_addr(bar)), "r"(count) : "memory");
+}
+__device__ __forceinline__ pk::FieldPar lds_par_a(uint32_t a) {
+  pk::FieldPar r;
+  asm volatile("ld.shared.v4.u32 {%0, %1, %2, %3}, [%4];" : "=r"(r.x), "=r"(r.y), "=r"(r.z), "=r"(r.w) : "r"(a));
+  return r;
 }
 
 // the transpose reduction of 16 per-lane values over a warp: afterwards lane
@@ -411,6 +436,176 @@ __device__ __forceinline__ AT warp_transpose_reduce(AT d[16], int lane) {
   return h + __shfl_xor_sync(0xFFFFFFFFu, h, 1);
 }
 
+// tile-body specialisations (per segment): every group present on its first
+// candidate pair, groups on the group path (the common rate layout); DC and
+// c = 1, 2 only (the common precision / accuracy layout); anything else
+enum { kSpecFull = 0, kSpecDC = 1, kSpecAny = 2 };
+
+// One tile of a fast segment from shared memory: adds 2^k (Q u) of the
+// lane's block in each of the four block-rows to s[h][r].
+// tw: the stage address of the lane's first record word (16 * lane added);
+// uw: the stage address of the lane's U entry; par: the warp's parameters.
+template <int SPEC>
+__device__ __forceinline__ void p2_tile(uint32_t tw, uint32_t uw, uint32_t par, bool k2, bool hasA, bool gA,
+                                        bool kA, bool hasB, bool gB, bool kB, int We, uint32_t ebase_bits,
+                                        float2 s[2][4]) {
+  constexpr int NW = SPEC == kSpecDC ? 2 : SPEC == kSpecFull ? 4 : pk::kFastWords;   // record words read
+  float u[4];
+  {
+    uint4 t;
+    asm volatile("ld.shared.v4.u32 {%0, %1, %2, %3}, [%4];" : "=r"(t.x), "=r"(t.y), "=r"(t.z), "=r"(t.w) : "r"(uw));
+    u[0] = __uint_as_float(t.x);
+    u[1] = __uint_as_float(t.y);
+    u[2] = __uint_as_float(t.z);
+    u[3] = __uint_as_float(t.w);
+  }
+  // a[i][k]: word k of block-row i's record (one 16-byte load per word;
+  // words past the record are stale and only ever shifted out)
+  uint32_t a[4][pk::kFastWords];
+#pragma unroll
+  for (int kw = 0; kw < pk::kFastWords; ++kw) {
+    if (kw < NW) {
+      uint4 t;
+      asm volatile("ld.shared.v4.u32 {%0, %1, %2, %3}, [%4];"
+                   : "=r"(t.x), "=r"(t.y), "=r"(t.z), "=r"(t.w) : "r"(tw + 512 * kw));
+      a[0][kw] = t.x;
+      a[1][kw] = t.y;
+      a[2][kw] = t.z;
+      a[3][kw] = t.w;
+    } else {
+      a[0][kw] = a[1][kw] = a[2][kw] = a[3][kw] = 0u;
+    }
+  }
+  // w[h][r] = (w of block-row 2h, of block-row 2h + 1), row r
+  float2 w[2][4];
+  {
+    const pk::FieldPar p0 = lds_par_a(par);
+#pragma unroll
+    for (int h = 0; h < 2; ++h) {
+      const float f0a = __int2float_rn(pk::field_dc(a[2 * h][0], a[2 * h][1], p0));
+      const float f0b = __int2float_rn(pk::field_dc(a[2 * h + 1][0], a[2 * h + 1][1], p0));
+      w[h][0] = __fmul2_rn(make_float2(f0a, f0b), make_float2(u[0], u[0]));
+      w[h][1] = w[h][2] = w[h][3] = make_float2(0.0f, 0.0f);
+    }
+  }
+  // Each field's parameters are loaded (shared memory, volatile) one field
+  // ahead of its use so the load latency hides behind the previous field.
+  // c = 1, 2: integer fields (up to 28 bits), binary32 by rounding
+  auto field_int = [&](auto C, auto K, const pk::FieldPar& p) {
+    constexpr int c = decltype(C)::value, kk = decltype(K)::value;
+    constexpr int r = seq_pos(c) >> 2, j = seq_pos(c) & 3;
+#pragma unroll
+    for (int h = 0; h < 2; ++h) {
+      const float2 q = make_float2(__int2float_rn(pk::field_i(a[2 * h][kk], a[2 * h][kk + 1], p)),
+                                   __int2float_rn(pk::field_i(a[2 * h + 1][kk], a[2 * h + 1][kk + 1], p)));
+      w[h][r] = __ffma2_rn(q, make_float2(u[j], u[j]), w[h][r]);
+    }
+  };
+  // c >= 3, field path: two funnel shifts put the field under the binary32
+  // exponent of 2^23, FADD2 removes 2^23 + 2^(W-1): exact
+  auto field = [&](auto C, auto K, const pk::FieldPar& p) {
+    constexpr int c = decltype(C)::value, kk = decltype(K)::value;
+    constexpr int r = seq_pos(c) >> 2, j = seq_pos(c) & 3;
+    const float off = __uint_as_float(p.w);
+#pragma unroll
+    for (int h = 0; h < 2; ++h) {
+      const uint32_t fa = fsr(pk::fsl64(a[2 * h][kk], a[2 * h][kk + 1], p.x), p.y, p.z);
+      const uint32_t fb = fsr(pk::fsl64(a[2 * h + 1][kk], a[2 * h + 1][kk + 1], p.x), p.y, p.z);
+      const float2 q = __fadd2_rn(make_float2(__uint_as_float(fa), __uint_as_float(fb)), make_float2(off, off));
+      w[h][r] = __ffma2_rn(q, make_float2(u[j], u[j]), w[h][r]);
+    }
+  };
+  // c >= 3, group path: the group's bits at the bottom of a register (one
+  // 64-bit shift per row), one LOP3 per field, one FFMA2 converts two rows
+  struct X4 {
+    uint32_t v0, v1, v2, v3;
+  };
+  auto fieldg = [&](auto C, const X4& x, const pk::FieldPar& p) {
+    constexpr int c = decltype(C)::value;
+    constexpr int r = seq_pos(c) >> 2, j = seq_pos(c) & 3;
+    const float sc2 = __uint_as_float(p.y), off = __uint_as_float(p.z);
+    const uint32_t f0 = (x.v0 & p.x) | pk::kMagic, f1 = (x.v1 & p.x) | pk::kMagic;
+    const uint32_t f2 = (x.v2 & p.x) | pk::kMagic, f3 = (x.v3 & p.x) | pk::kMagic;
+    const float2 q0 = __ffma2_rn(make_float2(__uint_as_float(f0), __uint_as_float(f1)), make_float2(sc2, sc2),
+                                 make_float2(off, off));
+    const float2 q1 = __ffma2_rn(make_float2(__uint_as_float(f2), __uint_as_float(f3)), make_float2(sc2, sc2),
+                                 make_float2(off, off));
+    w[0][r] = __ffma2_rn(q0, make_float2(u[j], u[j]), w[0][r]);
+    w[1][r] = __ffma2_rn(q1, make_float2(u[j], u[j]), w[1][r]);
+  };
+  // fields c0..c1 in order, parameters one field ahead; G: group path
+  auto run = [&](auto C0, auto C1, auto K, auto G) {
+    constexpr int c0 = decltype(C0)::value, c1 = decltype(C1)::value, kk = decltype(K)::value;
+    constexpr bool grp = decltype(G)::value;
+    pk::FieldPar p = lds_par_a(par + 16 * c0);
+    X4 x{};
+    if constexpr (grp) {
+      x.v0 = pk::group_bits(a[0][kk], a[0][kk + 1], p.w);
+      x.v1 = pk::group_bits(a[1][kk], a[1][kk + 1], p.w);
+      x.v2 = pk::group_bits(a[2][kk], a[2][kk + 1], p.w);
+      x.v3 = pk::group_bits(a[3][kk], a[3][kk + 1], p.w);
+    }
+    unroll_range<c0, c1>([&](auto CC) {
+      constexpr int c = decltype(CC)::value;
+      pk::FieldPar pn = p;
+      if constexpr (c < c1) pn = lds_par_a(par + 16 * (c + 1));
+      if constexpr (grp) fieldg(CC, x, p);
+      else if constexpr (c <= 2) field_int(CC, K, p);
+      else field(CC, K, p);
+      p = pn;
+    });
+  };
+  using I0 = std::integral_constant<int, 0>;
+  using I1 = std::integral_constant<int, 1>;
+  using I2 = std::integral_constant<int, 2>;
+  using I3 = std::integral_constant<int, 3>;
+  using T_ = std::true_type;
+  using F_ = std::false_type;
+  using C1_ = std::integral_constant<int, 1>;
+  using C2_ = std::integral_constant<int, 2>;
+  using C3_ = std::integral_constant<int, 3>;
+  using C8_ = std::integral_constant<int, 8>;
+  using C9_ = std::integral_constant<int, 9>;
+  using C15_ = std::integral_constant<int, 15>;
+  run(C1_(), C1_(), I0(), F_());
+  if (SPEC != kSpecAny) {
+    run(C2_(), C2_(), I0(), F_());
+    if (SPEC == kSpecFull) {
+      run(C3_(), C8_(), I1(), T_());
+      run(C9_(), C15_(), I2(), T_());
+    }
+  } else {
+    if (k2) run(C2_(), C2_(), I1(), F_());
+    else run(C2_(), C2_(), I0(), F_());
+    if (hasA) {
+      if (gA) {
+        if (kA) run(C3_(), C8_(), I2(), T_());
+        else run(C3_(), C8_(), I1(), T_());
+      } else {
+        if (kA) run(C3_(), C8_(), I2(), F_());
+        else run(C3_(), C8_(), I1(), F_());
+      }
+    }
+    if (hasB) {
+      if (gB) {
+        if (kB) run(C9_(), C15_(), I3(), T_());
+        else run(C9_(), C15_(), I2(), T_());
+      } else {
+        if (kB) run(C9_(), C15_(), I3(), F_());
+        else run(C9_(), C15_(), I2(), F_());
+      }
+    }
+  }
+#pragma unroll
+  for (int h = 0; h < 2; ++h) {
+    const uint32_t ea = pk::field_edelta(a[2 * h][0], We), eb = pk::field_edelta(a[2 * h + 1][0], We);
+    const float2 sc = make_float2(__uint_as_float(ebase_bits + (ea << 23)), __uint_as_float(ebase_bits + (eb << 23)));
+    // s += w 2^k: the product is exact, one rounding per term
+#pragma unroll
+    for (int r = 0; r < 4; ++r) s[h][r] = __ffma2_rn(w[h][r], sc, s[h][r]);
+  }
+}
+
 template <int POL>
 __global__ void __launch_bounds__(32 * kP2Warps, WHFF_P2_MINB) k_pk_gemv2(PkTable T, unsigned long long* status) {
   using AT = typename PkAcc<POL>::T;
@@ -432,9 +627,10 @@ __global__ void __launch_bounds__(32 * kP2Warps, WHFF_P2_MINB) k_pk_gemv2(PkTabl
   const int vw = part * kP2Warps + warp;
   const int nseg = P.g.nsegb > (uint64_t)vw ? (int)((P.g.nsegb - 1 - vw) / kVW + 1) : 0;
   const pk::Seg* gsegs = P.segs + band * P.g.nsegb + vw;
+  const pk::FieldPar* gpars = P.pars + (band * P.g.nsegb + vw) * 16;
 
   // segment headers -> a shared-memory ring, kP2HdrChunk at a time (the
-  // producer runs at most kP2Stages tiles -- so at most kP2Stages segments --
+  // producer runs at most kP2Stages items -- so at most kP2Stages segments --
   // ahead of the consumer: a header is never overwritten while needed)
   int hdr_loaded = 0;
   auto ensure_hdr = [&](int k) {
@@ -457,12 +653,13 @@ __global__ void __launch_bounds__(32 * kP2Warps, WHFF_P2_MINB) k_pk_gemv2(PkTabl
   uint64_t policy;
   asm volatile("createpolicy.fractional.L2::evict_first.b64 %0, 1.0;" : "=l"(policy));
 
-  // shared-memory addresses (32-bit) of the warp's stages and barriers
+  // shared-memory addresses (32-bit) of the warp's stages, barriers, parameters
   const uint32_t st0 = smem_addr(&W.stage[0][0]);
   const uint32_t bar0 = smem_addr(&W.bar[0]);
+  const uint32_t par0 = smem_addr(&W.par[0]);
 
   // producer: lane 0 issues; the cursor (segment pk, tile pt) is warp-uniform.
-  // Per segment: its body, tile size and first column; per tile: offsets.
+  // Per segment: its body, tile size and first column; per item: offsets.
   int pk = 0, pt = 0, pslot = 0, pntl = 0;
   uint32_t ptw = 0;
   const uint32_t* pbody = nullptr;
@@ -484,22 +681,23 @@ __global__ void __launch_bounds__(32 * kP2Warps, WHFF_P2_MINB) k_pk_gemv2(PkTabl
   };
   auto issue = [&]() {
     if (pk >= nseg) return;
+    const int nt = pntl - pt < kP2ItemTiles ? pntl - pt : kP2ItemTiles;
     if (lane == 0) {
-      const uint32_t ncol = (uint32_t)bc - pcol0 < (uint32_t)pk::kTile ? (uint32_t)bc - pcol0 : (uint32_t)pk::kTile;
       const uint32_t st = st0 + pslot * kP2StageBytes, bar = bar0 + 8 * pslot;
-      asm volatile("mbarrier.arrive.expect_tx.shared::cta.b64 _, [%0], %1;" ::"r"(bar), "r"(ptw * 4 + ncol * 16)
-                   : "memory");
+      const uint32_t tb = (uint32_t)nt * ptw * 4, ub = (uint32_t)nt * (pk::kTile * 16);   // U is padded
+      asm volatile("mbarrier.arrive.expect_tx.shared::cta.b64 _, [%0], %1;" ::"r"(bar), "r"(tb + ub) : "memory");
       asm volatile(
           "cp.async.bulk.shared::cluster.global.mbarrier::complete_tx::bytes.L2::cache_hint [%0], [%1], %2, [%3], %4;"
-          ::"r"(st), "l"(pbody), "r"(ptw * 4), "r"(bar), "l"(policy) : "memory");
+          ::"r"(st), "l"(pbody), "r"(tb), "r"(bar), "l"(policy) : "memory");
       asm volatile(
           "cp.async.bulk.shared::cluster.global.mbarrier::complete_tx::bytes.L2::cache_hint [%0], [%1], %2, [%3], %4;"
-          ::"r"(st + kP2TileBytes), "l"(U + pcol0), "r"(ncol * 16), "r"(bar), "l"(policy) : "memory");
+          ::"r"(st + kP2ItemTiles * kP2TileBytes), "l"(U + pcol0), "r"(ub), "r"(bar), "l"(policy) : "memory");
     }
     pslot = pslot + 1 == kP2Stages ? 0 : pslot + 1;
-    if (++pt < pntl) {
-      pbody += ptw;
-      pcol0 += pk::kTile;
+    pt += nt;
+    if (pt < pntl) {
+      pbody += nt * ptw;
+      pcol0 += nt * pk::kTile;
     } else {
       ++pk;
       pt = 0;
@@ -509,6 +707,10 @@ __global__ void __launch_bounds__(32 * kP2Warps, WHFF_P2_MINB) k_pk_gemv2(PkTabl
   skip();
   for (int i = 0; i < kP2Stages; ++i) issue();
 
+  // the next fast segment's parameters, prefetched (lanes 0..15)
+  pk::FieldPar pnext{0u, 0u, 0u, 0u};
+  if (lane < 16 && nseg > 0) pnext = gpars[lane];
+
   AT acc = (AT)0;          // row (lane >> 1): the warp's binary64 (single: binary32) sum
   int cslot = 0;
   uint32_t cphase = 0;
@@ -516,11 +718,18 @@ __global__ void __launch_bounds__(32 * kP2Warps, WHFF_P2_MINB) k_pk_gemv2(PkTabl
   for (int k = 0; k < nseg; ++k) {
     const uint64_t sb = vw + (uint64_t)kVW * k;
     ensure_hdr(k);
-    const pk::Seg S = hdr(k);
-    const int L = pk::seg_L(S), R = pk::rec_words(L);
+    const pk::Seg& S = hdr(k);   // shared memory
+    const int L = pk::seg_L(S);
     const int We = pk::seg_We(S);
     const int ntl = pk::seg_tiles(P.g, sb);
     const uint32_t ebase_bits = ((uint32_t)pk::seg_emax_base(S) - 59u) << 23;   // binary32 2^(emax_base - 186)
+    // this segment's parameters -> shared memory; prefetch the next one's
+    __syncwarp();
+    if (lane < 16) {
+      W.par[lane] = pnext;
+      if (k + 1 < nseg) pnext = gpars[(uint64_t)kVW * 16 * (k + 1) + lane];
+    }
+    __syncwarp();
     // the segment's per-lane binary32 sums: s[h][r] = (block-row 2h, 2h + 1) x row r
     float2 s[2][4];
 #pragma unroll
@@ -528,17 +737,16 @@ __global__ void __launch_bounds__(32 * kP2Warps, WHFF_P2_MINB) k_pk_gemv2(PkTabl
 #pragma unroll
       for (int r = 0; r < 4; ++r) s[h][r] = make_float2(0.0f, 0.0f);
     if (!pk::seg_generic(S)) {
-      __syncwarp();
-      if (lane < 16) W.par[lane] = pk::field_param(S, lane);
-      __syncwarp();
       const bool k2 = pk::seg_k2(S), kA = pk::seg_kA(S), kB = pk::seg_kB(S);
+      const bool gA = pk::seg_gA(S), gB = pk::seg_gB(S);
       // fields 3..8: w[0] bits 15..29 and w[1] bits 0..14; 9..15: w[1] bits
       // 15..29 and w[2] bits 0..19
       const bool hasA = ((S.w[0] >> 15) & 0x7FFFu) != 0 || (S.w[1] & 0x7FFFu) != 0;
       const bool hasB = ((S.w[1] >> 15) & 0x7FFFu) != 0 || (S.w[2] & 0xFFFFFu) != 0;
-      const uint32_t col00 = (uint32_t)(sb * pk::kSegTiles * pk::kTile) + lane;
-      for (int tt = 0; tt < ntl; ++tt) {
-        {
+      const uint32_t twb = (uint32_t)pk::tile_words(L) * 4;   // bytes per tile
+      auto items = [&](auto SPECC) {
+        constexpr int SPEC = decltype(SPECC)::value;
+        for (int tt = 0; tt < ntl; tt += kP2ItemTiles) {
           const uint32_t bar = bar0 + 8 * cslot;
           asm volatile(
               "{\n"
@@ -547,116 +755,24 @@ __global__ void __launch_bounds__(32 * kP2Warps, WHFF_P2_MINB) k_pk_gemv2(PkTabl
               "mbarrier.try_wait.parity.shared::cta.b64 p, [%0], %1;\n"
               "@!p bra W2C_WAIT_%=;\n"
               "}\n" ::"r"(bar), "r"(cphase) : "memory");
-        }
-        const uint32_t st = st0 + cslot * kP2StageBytes + 16 * lane;
-        const bool active = col00 + tt * pk::kTile < (uint32_t)bc;
-        uint4 uw;
-        asm volatile("ld.shared.v4.u32 {%0, %1, %2, %3}, [%4];"
-                     : "=r"(uw.x), "=r"(uw.y), "=r"(uw.z), "=r"(uw.w) : "r"(st + kP2TileBytes));
-        const float u[4] = {active ? __uint_as_float(uw.x) : 0.0f, active ? __uint_as_float(uw.y) : 0.0f,
-                            active ? __uint_as_float(uw.z) : 0.0f, active ? __uint_as_float(uw.w) : 0.0f};
-        // a[i][k]: word k of block-row i's record (one 16-byte load per word;
-        // words past the record are stale and only ever shifted out)
-        uint32_t a[4][pk::kFastWords];
+          const uint32_t st = st0 + cslot * kP2StageBytes + 16 * lane;
+          const int nt = ntl - tt < kP2ItemTiles ? ntl - tt : kP2ItemTiles;
 #pragma unroll
-        for (int kw = 0; kw < pk::kFastWords; ++kw) {
-          uint4 t;
-          asm volatile("ld.shared.v4.u32 {%0, %1, %2, %3}, [%4];"
-                       : "=r"(t.x), "=r"(t.y), "=r"(t.z), "=r"(t.w) : "r"(st + 512 * kw));
-          a[0][kw] = t.x;
-          a[1][kw] = t.y;
-          a[2][kw] = t.z;
-          a[3][kw] = t.w;
-        }
-        (void)R;
-
-        // w[h][r] = (w of block-row 2h, of block-row 2h + 1), row r
-        float2 w[2][4];
-        {
-          const pk::FieldPar p0 = lds_par(&W.par[0]);
-#pragma unroll
-          for (int h = 0; h < 2; ++h) {
-            const float f0a = __int2float_rn(pk::field_dc(a[2 * h][0], a[2 * h][1], p0));
-            const float f0b = __int2float_rn(pk::field_dc(a[2 * h + 1][0], a[2 * h + 1][1], p0));
-            w[h][0] = __fmul2_rn(make_float2(f0a, f0b), make_float2(u[0], u[0]));
-            w[h][1] = w[h][2] = w[h][3] = make_float2(0.0f, 0.0f);
+          for (int it = 0; it < kP2ItemTiles; ++it) {
+            if (it < nt)
+              p2_tile<SPEC>(st + it * twb, st + kP2ItemTiles * kP2TileBytes + it * (pk::kTile * 16), par0, k2,
+                            hasA, gA, kA, hasB, gB, kB, We, ebase_bits, s);
           }
+          // every lane has consumed the stage: refill it with the item kP2Stages ahead
+          __syncwarp();
+          issue();
+          cslot = cslot + 1 == kP2Stages ? 0 : cslot + 1;
+          cphase ^= cslot == 0 ? 1u : 0u;
         }
-        // c = 1, 2: integer fields (up to 28 bits), binary32 by rounding
-        auto field_int = [&](auto C, auto K) {
-          constexpr int c = decltype(C)::value, kk = decltype(K)::value;
-          constexpr int r = seq_pos(c) >> 2, j = seq_pos(c) & 3;
-          const pk::FieldPar p = lds_par(&W.par[c]);
-#pragma unroll
-          for (int h = 0; h < 2; ++h) {
-            const float2 q = make_float2(__int2float_rn(pk::field_i(a[2 * h][kk], a[2 * h][kk + 1], p)),
-                                         __int2float_rn(pk::field_i(a[2 * h + 1][kk], a[2 * h + 1][kk + 1], p)));
-            w[h][r] = __ffma2_rn(q, make_float2(u[j], u[j]), w[h][r]);
-          }
-        };
-        // c >= 3: magic-number binary32, exact
-        auto field = [&](auto C, auto K) {
-          constexpr int c = decltype(C)::value, kk = decltype(K)::value;
-          constexpr int r = seq_pos(c) >> 2, j = seq_pos(c) & 3;
-          const pk::FieldPar p = lds_par(&W.par[c]);
-          const float off = __uint_as_float(p.w);
-#pragma unroll
-          for (int h = 0; h < 2; ++h) {
-            const uint32_t fa = fsr(pk::fsl64(a[2 * h][kk], a[2 * h][kk + 1], p.x), p.y, p.z);
-            const uint32_t fb = fsr(pk::fsl64(a[2 * h + 1][kk], a[2 * h + 1][kk + 1], p.x), p.y, p.z);
-            const float2 q = __fadd2_rn(make_float2(__uint_as_float(fa), __uint_as_float(fb)), make_float2(off, off));
-            w[h][r] = __ffma2_rn(q, make_float2(u[j], u[j]), w[h][r]);
-          }
-        };
-        using I0 = std::integral_constant<int, 0>;
-        using I1 = std::integral_constant<int, 1>;
-        using I2 = std::integral_constant<int, 2>;
-        using I3 = std::integral_constant<int, 3>;
-        field_int(std::integral_constant<int, 1>(), I0());
-        if (k2) field_int(std::integral_constant<int, 2>(), I1());
-        else field_int(std::integral_constant<int, 2>(), I0());
-        auto groupA = [&](auto K) {
-          field(std::integral_constant<int, 3>(), K);
-          field(std::integral_constant<int, 4>(), K);
-          field(std::integral_constant<int, 5>(), K);
-          field(std::integral_constant<int, 6>(), K);
-          field(std::integral_constant<int, 7>(), K);
-          field(std::integral_constant<int, 8>(), K);
-        };
-        auto groupB = [&](auto K) {
-          field(std::integral_constant<int, 9>(), K);
-          field(std::integral_constant<int, 10>(), K);
-          field(std::integral_constant<int, 11>(), K);
-          field(std::integral_constant<int, 12>(), K);
-          field(std::integral_constant<int, 13>(), K);
-          field(std::integral_constant<int, 14>(), K);
-          field(std::integral_constant<int, 15>(), K);
-        };
-        if (hasA) {
-          if (kA) groupA(I2());
-          else groupA(I1());
-        }
-        if (hasB) {
-          if (kB) groupB(I3());
-          else groupB(I2());
-        }
-        // every lane has consumed the stage: refill it with the tile kP2Stages ahead
-        __syncwarp();
-        issue();
-        cslot = cslot + 1 == kP2Stages ? 0 : cslot + 1;
-        cphase ^= cslot == 0 ? 1u : 0u;
-#pragma unroll
-        for (int h = 0; h < 2; ++h) {
-          const uint32_t ea = pk::field_edelta(a[2 * h][0], We), eb = pk::field_edelta(a[2 * h + 1][0], We);
-          // (lanes past the row end: scale 0)
-          const float2 sc = active ? make_float2(__uint_as_float(ebase_bits + (ea << 23)),
-                                                 __uint_as_float(ebase_bits + (eb << 23)))
-                                   : make_float2(0.0f, 0.0f);
-          // s += w 2^k: the product is exact, one rounding per term
-#pragma unroll
-          for (int r = 0; r < 4; ++r) s[h][r] = __ffma2_rn(w[h][r], sc, s[h][r]);
-        }
-      }
+      };
+      if (!k2 && hasA && gA && !kA && hasB && gB && !kB) items(std::integral_constant<int, kSpecFull>());
+      else if (!k2 && !hasA && !hasB) items(std::integral_constant<int, kSpecDC>());
+      else items(std::integral_constant<int, kSpecAny>());
     } else {
       // generic segment (not staged): per-lane sequential parse from global memory
       const uint64_t TW = pk::tile_words(L);

@@ -47,6 +47,9 @@
 // Everything the packer and the kernels share is __host__ __device__.
 #pragma once
 
+#include <cmath>
+#include <cstring>
+
 #include "whff_decode.cuh"
 
 namespace whff {
@@ -66,6 +69,7 @@ constexpr uint32_t kMagic = 0x4B000000u;                      // binary32 2^23
 struct alignas(16) Seg {
   uint64_t body;       // word offset of the segment body
   uint32_t hdr;        // [0:9) emax_base [9:13) W_e [13] generic [14] k2 [15] kA [16:25) L [25] kB
+                       // [26] gA [27] gB (group path: the group spans <= 23 bits)
   uint32_t w[3];       // W_c, 5 bits each: c = 6 * word + slot
   uint32_t o[4];       // fast path: offset of field c (8 bits): c = 4 * word + slot
   uint32_t exc_begin;  // first exception of the segment
@@ -78,6 +82,8 @@ WHFF_HD bool seg_generic(const Seg& s) { return (s.hdr >> 13) & 1u; }
 WHFF_HD bool seg_k2(const Seg& s) { return (s.hdr >> 14) & 1u; }
 WHFF_HD bool seg_kA(const Seg& s) { return (s.hdr >> 15) & 1u; }
 WHFF_HD bool seg_kB(const Seg& s) { return (s.hdr >> 25) & 1u; }
+WHFF_HD bool seg_gA(const Seg& s) { return (s.hdr >> 26) & 1u; }
+WHFF_HD bool seg_gB(const Seg& s) { return (s.hdr >> 27) & 1u; }
 WHFF_HD int seg_L(const Seg& s) { return (int)((s.hdr >> 16) & 511u); }
 WHFF_HD int seg_W(const Seg& s, int c) { return (int)((s.w[c / 6] >> (5 * (c % 6))) & 31u); }
 WHFF_HD int seg_o(const Seg& s, int c) { return (int)((s.o[c / 4] >> (8 * (c % 4))) & 255u); }
@@ -95,7 +101,7 @@ WHFF_HD int field_pair(int c, bool k2, bool kA, bool kB) {
 // c >= 3 is wider than the magic path allows, or L > 160.
 struct Layout {
   int We, L;
-  bool fast, k2, kA, kB;
+  bool fast, k2, kA, kB, gA, gB;
   int o[16];
 };
 WHFF_HD bool place_group(const int W[16], int c0, int c1, int k, int& cur, int o[16]) {
@@ -143,12 +149,18 @@ WHFF_HD void make_layout(int We, const int W[16], Layout& f) {
   f.We = We;
   f.L = cur;
   f.fast = fast;
+  int wa = 0, wb = 0;
+  for (int c = 3; c <= 8; ++c) wa += W[c];
+  for (int c = 9; c < 16; ++c) wb += W[c];
+  f.gA = fast && wa <= kMagicW;
+  f.gB = fast && wb <= kMagicW;
 }
 
 // segment header word from a layout
 WHFF_HD uint32_t seg_hdr(uint32_t ebase, const Layout& f) {
   return ebase | ((uint32_t)f.We << 9) | ((f.fast ? 0u : 1u) << 13) | ((f.k2 ? 1u : 0u) << 14) |
-         ((f.kA ? 1u : 0u) << 15) | ((uint32_t)f.L << 16) | ((f.kB ? 1u : 0u) << 25);
+         ((f.kA ? 1u : 0u) << 15) | ((uint32_t)f.L << 16) | ((f.kB ? 1u : 0u) << 25) |
+         ((f.gA ? 1u : 0u) << 26) | ((f.gB ? 1u : 0u) << 27);
 }
 
 // signed width: the fewest bits holding q in two's complement / offset binary
@@ -296,6 +308,67 @@ WHFF_HD FieldPar field_param(const Seg& S, int c) {
     p.w = c <= 2 ? 1u << (W - 1) : 0xCB000000u + (1u << (W - 1));   // -(2^23 + 2^(W-1))
   }
   return p;
+}
+
+// Group extraction (c = 3..8 "A", 9..15 "B"), used when a group's fields
+// span at most 23 bits together: one 64-bit right shift brings the whole
+// group to the bottom of a register (x = (hi:lo) >> n), then each field is
+// one LOP3 -- (x & mask) | 2^23-exponent -- giving the binary32 value
+// 2^23 + u 2^s exactly, and q = value 2^-s - (2^(23-s) + 2^(W-1)) exactly
+// (one FMA: every intermediate is an exact binary32 integer).  Parameters:
+// {mask = (2^W - 1) << s, bits of 2^-s, bits of -(2^(23-s) + 2^(W-1)), n};
+// absent fields {0, 1.0, -2^23, n} give q = 0.
+WHFF_HD constexpr int group_first(int g) { return g == 0 ? 3 : 9; }
+WHFF_HD constexpr int group_last(int g) { return g == 0 ? 8 : 15; }
+WHFF_HD uint32_t f32_bits(float x) {
+#if defined(__CUDA_ARCH__)
+  return __float_as_uint(x);
+#else
+  uint32_t u;
+  std::memcpy(&u, &x, 4);
+  return u;
+#endif
+}
+WHFF_HD int group_width(const Seg& S, int g) {
+  int w = 0;
+  for (int c = group_first(g); c <= group_last(g); ++c) w += seg_W(S, c);
+  return w;
+}
+WHFF_HD bool group_magic(const Seg& S, int g) { return g == 0 ? seg_gA(S) : seg_gB(S); }
+WHFF_HD FieldPar group_param(const Seg& S, int c) {
+  const int g = c <= 8 ? 0 : 1;
+  const int k = field_pair(c, seg_k2(S), seg_kA(S), seg_kB(S));
+  int end = 0;   // end bit (exclusive) of the group inside the pair window
+  for (int cc = group_first(g); cc <= group_last(g); ++cc) {
+    const int Wc = seg_W(S, cc);
+    if (Wc && seg_o(S, cc) - 32 * k + Wc > end) end = seg_o(S, cc) - 32 * k + Wc;
+  }
+  FieldPar p;
+  p.w = end ? (uint32_t)(64 - end) : 0u;
+  const int W = seg_W(S, c);
+  const int sh = W ? end - (seg_o(S, c) - 32 * k + W) : 0;
+  p.x = W ? ((W >= 32 ? 0xFFFFFFFFu : ((1u << W) - 1u)) << sh) : 0u;
+  p.y = (uint32_t)(127 - sh) << 23;                            // 2^-sh
+  p.z = W ? 0x80000000u | f32_bits((float)((1u << (23 - sh)) + (1u << (W - 1)))) : 0xCB000000u;
+  return p;
+}
+// the parameters k_pk_gemv2 uses for field c of a fast segment (the packer
+// stores them per segment: whff_dstream_pack)
+WHFF_HD FieldPar seg_param(const Seg& S, int c) {
+  return (c >= 3 && group_magic(S, c <= 8 ? 0 : 1)) ? group_param(S, c) : field_param(S, c);
+}
+
+// the group bits at the bottom of a register
+WHFF_HD uint32_t group_bits(uint32_t hi, uint32_t lo, uint32_t n) {
+  return (uint32_t)((((uint64_t)hi << 32) | lo) >> n);
+}
+WHFF_HD float group_field_f(uint32_t x, const FieldPar& p) {
+  const uint32_t b = (x & p.x) | kMagic;
+#if defined(__CUDA_ARCH__)
+  return __fmaf_rn(__uint_as_float(b), __uint_as_float(p.y), __uint_as_float(p.z));
+#else
+  return std::fma(as_float(b), as_float(p.y), as_float(p.z));
+#endif
 }
 
 // high word of the 64-bit (hi:lo) << n, n in [0, 63]: one SHF.L.U64.HI

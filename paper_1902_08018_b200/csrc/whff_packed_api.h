@@ -14,6 +14,7 @@
 struct PkView {
   const uint32_t* body;
   const whff::pk::Seg* segs;          // [band][segment]
+  const whff::pk::FieldPar* pars;     // [band][segment][16]: seg_param (k_pk_gemv2)
   const uint64_t* exc_block;    // [exception] block index (row-major blocks)
   const uint32_t* exc_words;    // [exception][16] binary32 words, raster order
   whff::pk::Geom g;
@@ -55,6 +56,11 @@ constexpr int kPkSplit = kPkVW / kPkWarps;  // CTAs per band
 // host launchers (whff_packed.cu); all asynchronous on `cs`
 cudaError_t pk_launch_stats(const struct StreamView& s, const whff::pk::Geom& g, whff::pk::Seg* segs,
                             uint64_t* seg_words, uint64_t* seg_exc, cudaStream_t cs);
+// segment headers followed by the per-segment parameter tables
+inline uint64_t pk_segs_bytes(uint64_t nseg) {
+  return nseg * (sizeof(whff::pk::Seg) + 16 * sizeof(whff::pk::FieldPar));
+}
+cudaError_t pk_launch_params(whff::pk::Seg* segs, uint64_t nseg, cudaStream_t cs);
 cudaError_t pk_launch_finalize(whff::pk::Seg* segs, uint64_t nseg, const uint64_t* off, const uint64_t* eoff,
                                cudaStream_t cs);
 cudaError_t pk_launch_emit(const struct StreamView& s, const whff::pk::Geom& g, const whff::pk::Seg* segs,

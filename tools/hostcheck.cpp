@@ -384,6 +384,15 @@ int64_t hc_unpack(const uint8_t* segs_in, const uint32_t* body, const uint64_t* 
               const int k = pk::field_pair(c, pk::seg_k2(S), pk::seg_kA(S), pk::seg_kB(S));
               same = same && pk::field_f(a[k], k + 1 < pk::kFastWords ? a[k + 1] : 0u, par[c]) == (float)q[c];
             }
+            // the group path (k_pk_gemv2, groups of <= 23 bits) gives the same q
+            for (int gg = 0; gg < 2; ++gg) {
+              if (!pk::group_magic(S, gg)) continue;
+              const int k = pk::field_pair(pk::group_first(gg), pk::seg_k2(S), pk::seg_kA(S), pk::seg_kB(S));
+              const uint32_t x = pk::group_bits(a[k], k + 1 < pk::kFastWords ? a[k + 1] : 0u,
+                                                pk::group_param(S, pk::group_first(gg)).w);
+              for (int c = pk::group_first(gg); c <= pk::group_last(gg); ++c)
+                same = same && pk::group_field_f(x, pk::group_param(S, c)) == (float)q[c];
+            }
             if (!same) ++bad;
           }
           float x[16];
