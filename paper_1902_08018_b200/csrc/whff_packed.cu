@@ -488,29 +488,40 @@ __device__ __forceinline__ void p2_tile(uint32_t tw, uint32_t uw, uint32_t par, 
       w[h][1] = w[h][2] = w[h][3] = make_float2(0.0f, 0.0f);
     }
   }
+  // kSpecAny: the pair of a group chosen per segment, selected into b[][]
+  uint32_t b[4][2];
+  // the pair (hi, lo) of row i for a field: a[i][kk], a[i][kk + 1], or b[i][]
+  auto hi = [&](auto K, auto B, int i) -> uint32_t {
+    if constexpr (decltype(B)::value) return b[i][0];
+    else return a[i][decltype(K)::value];
+  };
+  auto lo = [&](auto K, auto B, int i) -> uint32_t {
+    if constexpr (decltype(B)::value) return b[i][1];
+    else return a[i][decltype(K)::value + 1];
+  };
   // Each field's parameters are loaded (shared memory, volatile) one field
   // ahead of its use so the load latency hides behind the previous field.
   // c = 1, 2: integer fields (up to 28 bits), binary32 by rounding
-  auto field_int = [&](auto C, auto K, const pk::FieldPar& p) {
-    constexpr int c = decltype(C)::value, kk = decltype(K)::value;
+  auto field_int = [&](auto C, auto K, auto B, const pk::FieldPar& p) {
+    constexpr int c = decltype(C)::value;
     constexpr int r = seq_pos(c) >> 2, j = seq_pos(c) & 3;
 #pragma unroll
     for (int h = 0; h < 2; ++h) {
-      const float2 q = make_float2(__int2float_rn(pk::field_i(a[2 * h][kk], a[2 * h][kk + 1], p)),
-                                   __int2float_rn(pk::field_i(a[2 * h + 1][kk], a[2 * h + 1][kk + 1], p)));
+      const float2 q = make_float2(__int2float_rn(pk::field_i(hi(K, B, 2 * h), lo(K, B, 2 * h), p)),
+                                   __int2float_rn(pk::field_i(hi(K, B, 2 * h + 1), lo(K, B, 2 * h + 1), p)));
       w[h][r] = __ffma2_rn(q, make_float2(u[j], u[j]), w[h][r]);
     }
   };
   // c >= 3, field path: two funnel shifts put the field under the binary32
   // exponent of 2^23, FADD2 removes 2^23 + 2^(W-1): exact
-  auto field = [&](auto C, auto K, const pk::FieldPar& p) {
-    constexpr int c = decltype(C)::value, kk = decltype(K)::value;
+  auto field = [&](auto C, auto K, auto B, const pk::FieldPar& p) {
+    constexpr int c = decltype(C)::value;
     constexpr int r = seq_pos(c) >> 2, j = seq_pos(c) & 3;
     const float off = __uint_as_float(p.w);
 #pragma unroll
     for (int h = 0; h < 2; ++h) {
-      const uint32_t fa = fsr(pk::fsl64(a[2 * h][kk], a[2 * h][kk + 1], p.x), p.y, p.z);
-      const uint32_t fb = fsr(pk::fsl64(a[2 * h + 1][kk], a[2 * h + 1][kk + 1], p.x), p.y, p.z);
+      const uint32_t fa = fsr(pk::fsl64(hi(K, B, 2 * h), lo(K, B, 2 * h), p.x), p.y, p.z);
+      const uint32_t fb = fsr(pk::fsl64(hi(K, B, 2 * h + 1), lo(K, B, 2 * h + 1), p.x), p.y, p.z);
       const float2 q = __fadd2_rn(make_float2(__uint_as_float(fa), __uint_as_float(fb)), make_float2(off, off));
       w[h][r] = __ffma2_rn(q, make_float2(u[j], u[j]), w[h][r]);
     }
@@ -534,31 +545,39 @@ __device__ __forceinline__ void p2_tile(uint32_t tw, uint32_t uw, uint32_t par, 
     w[1][r] = __ffma2_rn(q1, make_float2(u[j], u[j]), w[1][r]);
   };
   // fields c0..c1 in order, parameters one field ahead; G: group path
-  auto run = [&](auto C0, auto C1, auto K, auto G) {
-    constexpr int c0 = decltype(C0)::value, c1 = decltype(C1)::value, kk = decltype(K)::value;
+  auto run = [&](auto C0, auto C1, auto K, auto B, auto G) {
+    constexpr int c0 = decltype(C0)::value, c1 = decltype(C1)::value;
     constexpr bool grp = decltype(G)::value;
     pk::FieldPar p = lds_par_a(par + 16 * c0);
     X4 x{};
     if constexpr (grp) {
-      x.v0 = pk::group_bits(a[0][kk], a[0][kk + 1], p.w);
-      x.v1 = pk::group_bits(a[1][kk], a[1][kk + 1], p.w);
-      x.v2 = pk::group_bits(a[2][kk], a[2][kk + 1], p.w);
-      x.v3 = pk::group_bits(a[3][kk], a[3][kk + 1], p.w);
+      x.v0 = pk::group_bits(hi(K, B, 0), lo(K, B, 0), p.w);
+      x.v1 = pk::group_bits(hi(K, B, 1), lo(K, B, 1), p.w);
+      x.v2 = pk::group_bits(hi(K, B, 2), lo(K, B, 2), p.w);
+      x.v3 = pk::group_bits(hi(K, B, 3), lo(K, B, 3), p.w);
     }
     unroll_range<c0, c1>([&](auto CC) {
       constexpr int c = decltype(CC)::value;
       pk::FieldPar pn = p;
       if constexpr (c < c1) pn = lds_par_a(par + 16 * (c + 1));
       if constexpr (grp) fieldg(CC, x, p);
-      else if constexpr (c <= 2) field_int(CC, K, p);
-      else field(CC, K, p);
+      else if constexpr (c <= 2) field_int(CC, K, B, p);
+      else field(CC, K, B, p);
       p = pn;
     });
+  };
+  // b[i][] = pair kk (up: kk + 1) of row i
+  auto pick = [&](auto K, bool up) {
+    constexpr int kk = decltype(K)::value;
+#pragma unroll
+    for (int i = 0; i < 4; ++i) {
+      b[i][0] = up ? a[i][kk + 1] : a[i][kk];
+      b[i][1] = up ? a[i][kk + 2] : a[i][kk + 1];
+    }
   };
   using I0 = std::integral_constant<int, 0>;
   using I1 = std::integral_constant<int, 1>;
   using I2 = std::integral_constant<int, 2>;
-  using I3 = std::integral_constant<int, 3>;
   using T_ = std::true_type;
   using F_ = std::false_type;
   using C1_ = std::integral_constant<int, 1>;
@@ -567,33 +586,25 @@ __device__ __forceinline__ void p2_tile(uint32_t tw, uint32_t uw, uint32_t par, 
   using C8_ = std::integral_constant<int, 8>;
   using C9_ = std::integral_constant<int, 9>;
   using C15_ = std::integral_constant<int, 15>;
-  run(C1_(), C1_(), I0(), F_());
+  run(C1_(), C1_(), I0(), F_(), F_());
   if (SPEC != kSpecAny) {
-    run(C2_(), C2_(), I0(), F_());
+    run(C2_(), C2_(), I0(), F_(), F_());
     if (SPEC == kSpecFull) {
-      run(C3_(), C8_(), I1(), T_());
-      run(C9_(), C15_(), I2(), T_());
+      run(C3_(), C8_(), I1(), F_(), T_());
+      run(C9_(), C15_(), I2(), F_(), T_());
     }
   } else {
-    if (k2) run(C2_(), C2_(), I1(), F_());
-    else run(C2_(), C2_(), I0(), F_());
+    pick(I0(), k2);
+    run(C2_(), C2_(), I0(), T_(), F_());
     if (hasA) {
-      if (gA) {
-        if (kA) run(C3_(), C8_(), I2(), T_());
-        else run(C3_(), C8_(), I1(), T_());
-      } else {
-        if (kA) run(C3_(), C8_(), I2(), F_());
-        else run(C3_(), C8_(), I1(), F_());
-      }
+      pick(I1(), kA);
+      if (gA) run(C3_(), C8_(), I1(), T_(), T_());
+      else run(C3_(), C8_(), I1(), T_(), F_());
     }
     if (hasB) {
-      if (gB) {
-        if (kB) run(C9_(), C15_(), I3(), T_());
-        else run(C9_(), C15_(), I2(), T_());
-      } else {
-        if (kB) run(C9_(), C15_(), I3(), F_());
-        else run(C9_(), C15_(), I2(), F_());
-      }
+      pick(I2(), kB);
+      if (gB) run(C9_(), C15_(), I2(), T_(), T_());
+      else run(C9_(), C15_(), I2(), T_(), F_());
     }
   }
 #pragma unroll
@@ -757,9 +768,8 @@ __global__ void __launch_bounds__(32 * kP2Warps, WHFF_P2_MINB) k_pk_gemv2(PkTabl
               "}\n" ::"r"(bar), "r"(cphase) : "memory");
           const uint32_t st = st0 + cslot * kP2StageBytes + 16 * lane;
           const int nt = ntl - tt < kP2ItemTiles ? ntl - tt : kP2ItemTiles;
-#pragma unroll
-          for (int it = 0; it < kP2ItemTiles; ++it) {
-            if (it < nt)
+#pragma unroll 1
+          for (int it = 0; it < nt; ++it) {
               p2_tile<SPEC>(st + it * twb, st + kP2ItemTiles * kP2TileBytes + it * (pk::kTile * 16), par0, k2,
                             hasA, gA, kA, hasB, gB, kB, We, ebase_bits, s);
           }
