@@ -446,8 +446,8 @@ enum { kSpecFull = 0, kSpecDC = 1, kSpecAny = 2 };
 // tw: the stage address of the lane's first record word (16 * lane added);
 // uw: the stage address of the lane's U entry; par: the warp's parameters.
 template <int SPEC>
-__device__ __forceinline__ void p2_tile(uint32_t tw, uint32_t uw, uint32_t par, bool k2, bool hasA, bool gA,
-                                        bool kA, bool hasB, bool gB, bool kB, int We, uint32_t ebase_bits,
+__device__ __forceinline__ void p2_tile(uint32_t tw, uint32_t uw, uint32_t par, bool m12, bool k2, bool hasA,
+                                        bool gA, bool kA, bool hasB, bool gB, bool kB, int We, uint32_t ebase_bits,
                                         float2 s[2][4]) {
   constexpr int NW = SPEC == kSpecDC ? 2 : SPEC == kSpecFull ? 4 : pk::kFastWords;   // record words read
   float u[4];
@@ -544,8 +544,9 @@ __device__ __forceinline__ void p2_tile(uint32_t tw, uint32_t uw, uint32_t par, 
     w[0][r] = __ffma2_rn(q0, make_float2(u[j], u[j]), w[0][r]);
     w[1][r] = __ffma2_rn(q1, make_float2(u[j], u[j]), w[1][r]);
   };
-  // fields c0..c1 in order, parameters one field ahead; G: group path
-  auto run = [&](auto C0, auto C1, auto K, auto B, auto G) {
+  // fields c0..c1 in order, parameters one field ahead; G: group path; M:
+  // c = 1, 2 in the magic-number format (seg_m12)
+  auto run = [&](auto C0, auto C1, auto K, auto B, auto G, auto M) {
     constexpr int c0 = decltype(C0)::value, c1 = decltype(C1)::value;
     constexpr bool grp = decltype(G)::value;
     pk::FieldPar p = lds_par_a(par + 16 * c0);
@@ -561,7 +562,7 @@ __device__ __forceinline__ void p2_tile(uint32_t tw, uint32_t uw, uint32_t par, 
       pk::FieldPar pn = p;
       if constexpr (c < c1) pn = lds_par_a(par + 16 * (c + 1));
       if constexpr (grp) fieldg(CC, x, p);
-      else if constexpr (c <= 2) field_int(CC, K, B, p);
+      else if constexpr (c <= 2 && !decltype(M)::value) field_int(CC, K, B, p);
       else field(CC, K, B, p);
       p = pn;
     });
@@ -586,25 +587,27 @@ __device__ __forceinline__ void p2_tile(uint32_t tw, uint32_t uw, uint32_t par, 
   using C8_ = std::integral_constant<int, 8>;
   using C9_ = std::integral_constant<int, 9>;
   using C15_ = std::integral_constant<int, 15>;
-  run(C1_(), C1_(), I0(), F_(), F_());
   if (SPEC != kSpecAny) {
-    run(C2_(), C2_(), I0(), F_(), F_());
+    run(C1_(), C2_(), I0(), F_(), F_(), T_());
     if (SPEC == kSpecFull) {
-      run(C3_(), C8_(), I1(), F_(), T_());
-      run(C9_(), C15_(), I2(), F_(), T_());
+      run(C3_(), C8_(), I1(), F_(), T_(), F_());
+      run(C9_(), C15_(), I2(), F_(), T_(), F_());
     }
   } else {
+    if (m12) run(C1_(), C1_(), I0(), F_(), F_(), T_());
+    else run(C1_(), C1_(), I0(), F_(), F_(), F_());
     pick(I0(), k2);
-    run(C2_(), C2_(), I0(), T_(), F_());
+    if (m12) run(C2_(), C2_(), I0(), T_(), F_(), T_());
+    else run(C2_(), C2_(), I0(), T_(), F_(), F_());
     if (hasA) {
       pick(I1(), kA);
-      if (gA) run(C3_(), C8_(), I1(), T_(), T_());
-      else run(C3_(), C8_(), I1(), T_(), F_());
+      if (gA) run(C3_(), C8_(), I1(), T_(), T_(), F_());
+      else run(C3_(), C8_(), I1(), T_(), F_(), F_());
     }
     if (hasB) {
       pick(I2(), kB);
-      if (gB) run(C9_(), C15_(), I2(), T_(), T_());
-      else run(C9_(), C15_(), I2(), T_(), F_());
+      if (gB) run(C9_(), C15_(), I2(), T_(), T_(), F_());
+      else run(C9_(), C15_(), I2(), T_(), F_(), F_());
     }
   }
 #pragma unroll
@@ -749,7 +752,7 @@ __global__ void __launch_bounds__(32 * kP2Warps, WHFF_P2_MINB) k_pk_gemv2(PkTabl
       for (int r = 0; r < 4; ++r) s[h][r] = make_float2(0.0f, 0.0f);
     if (!pk::seg_generic(S)) {
       const bool k2 = pk::seg_k2(S), kA = pk::seg_kA(S), kB = pk::seg_kB(S);
-      const bool gA = pk::seg_gA(S), gB = pk::seg_gB(S);
+      const bool gA = pk::seg_gA(S), gB = pk::seg_gB(S), m12 = pk::seg_m12(S);
       // fields 3..8: w[0] bits 15..29 and w[1] bits 0..14; 9..15: w[1] bits
       // 15..29 and w[2] bits 0..19
       const bool hasA = ((S.w[0] >> 15) & 0x7FFFu) != 0 || (S.w[1] & 0x7FFFu) != 0;
@@ -770,8 +773,8 @@ __global__ void __launch_bounds__(32 * kP2Warps, WHFF_P2_MINB) k_pk_gemv2(PkTabl
           const int nt = ntl - tt < kP2ItemTiles ? ntl - tt : kP2ItemTiles;
 #pragma unroll 1
           for (int it = 0; it < nt; ++it) {
-              p2_tile<SPEC>(st + it * twb, st + kP2ItemTiles * kP2TileBytes + it * (pk::kTile * 16), par0, k2,
-                            hasA, gA, kA, hasB, gB, kB, We, ebase_bits, s);
+              p2_tile<SPEC>(st + it * twb, st + kP2ItemTiles * kP2TileBytes + it * (pk::kTile * 16), par0, m12,
+                            k2, hasA, gA, kA, hasB, gB, kB, We, ebase_bits, s);
           }
           // every lane has consumed the stage: refill it with the item kP2Stages ahead
           __syncwarp();
@@ -780,8 +783,8 @@ __global__ void __launch_bounds__(32 * kP2Warps, WHFF_P2_MINB) k_pk_gemv2(PkTabl
           cphase ^= cslot == 0 ? 1u : 0u;
         }
       };
-      if (!k2 && hasA && gA && !kA && hasB && gB && !kB) items(std::integral_constant<int, kSpecFull>());
-      else if (!k2 && !hasA && !hasB) items(std::integral_constant<int, kSpecDC>());
+      if (m12 && !k2 && hasA && gA && !kA && hasB && gB && !kB) items(std::integral_constant<int, kSpecFull>());
+      else if (m12 && !k2 && !hasA && !hasB) items(std::integral_constant<int, kSpecDC>());
       else items(std::integral_constant<int, kSpecAny>());
     } else {
       // generic segment (not staged): per-lane sequential parse from global memory

@@ -70,6 +70,8 @@ struct alignas(16) Seg {
   uint64_t body;       // word offset of the segment body
   uint32_t hdr;        // [0:9) emax_base [9:13) W_e [13] generic [14] k2 [15] kA [16:25) L [25] kB
                        // [26] gA [27] gB (group path: the group spans <= 23 bits)
+                       // [28] m12 (c = 1, 2 no wider than the magic path: k_pk_gemv2
+                       //      converts them like c >= 3)
   uint32_t w[3];       // W_c, 5 bits each: c = 6 * word + slot
   uint32_t o[4];       // fast path: offset of field c (8 bits): c = 4 * word + slot
   uint32_t exc_begin;  // first exception of the segment
@@ -84,6 +86,7 @@ WHFF_HD bool seg_kA(const Seg& s) { return (s.hdr >> 15) & 1u; }
 WHFF_HD bool seg_kB(const Seg& s) { return (s.hdr >> 25) & 1u; }
 WHFF_HD bool seg_gA(const Seg& s) { return (s.hdr >> 26) & 1u; }
 WHFF_HD bool seg_gB(const Seg& s) { return (s.hdr >> 27) & 1u; }
+WHFF_HD bool seg_m12(const Seg& s) { return (s.hdr >> 28) & 1u; }
 WHFF_HD int seg_L(const Seg& s) { return (int)((s.hdr >> 16) & 511u); }
 WHFF_HD int seg_W(const Seg& s, int c) { return (int)((s.w[c / 6] >> (5 * (c % 6))) & 31u); }
 WHFF_HD int seg_o(const Seg& s, int c) { return (int)((s.o[c / 4] >> (8 * (c % 4))) & 255u); }
@@ -101,7 +104,7 @@ WHFF_HD int field_pair(int c, bool k2, bool kA, bool kB) {
 // c >= 3 is wider than the magic path allows, or L > 160.
 struct Layout {
   int We, L;
-  bool fast, k2, kA, kB, gA, gB;
+  bool fast, k2, kA, kB, gA, gB, m12;
   int o[16];
 };
 WHFF_HD bool place_group(const int W[16], int c0, int c1, int k, int& cur, int o[16]) {
@@ -154,13 +157,14 @@ WHFF_HD void make_layout(int We, const int W[16], Layout& f) {
   for (int c = 9; c < 16; ++c) wb += W[c];
   f.gA = fast && wa <= kMagicW;
   f.gB = fast && wb <= kMagicW;
+  f.m12 = fast && W[1] <= kMagicW && W[2] <= kMagicW;
 }
 
 // segment header word from a layout
 WHFF_HD uint32_t seg_hdr(uint32_t ebase, const Layout& f) {
   return ebase | ((uint32_t)f.We << 9) | ((f.fast ? 0u : 1u) << 13) | ((f.k2 ? 1u : 0u) << 14) |
          ((f.kA ? 1u : 0u) << 15) | ((uint32_t)f.L << 16) | ((f.kB ? 1u : 0u) << 25) |
-         ((f.gA ? 1u : 0u) << 26) | ((f.gB ? 1u : 0u) << 27);
+         ((f.gA ? 1u : 0u) << 26) | ((f.gB ? 1u : 0u) << 27) | ((f.m12 ? 1u : 0u) << 28);
 }
 
 // signed width: the fewest bits holding q in two's complement / offset binary
@@ -355,7 +359,26 @@ WHFF_HD FieldPar group_param(const Seg& S, int c) {
 // the parameters k_pk_gemv2 uses for field c of a fast segment (the packer
 // stores them per segment: whff_dstream_pack)
 WHFF_HD FieldPar seg_param(const Seg& S, int c) {
-  return (c >= 3 && group_magic(S, c <= 8 ? 0 : 1)) ? group_param(S, c) : field_param(S, c);
+  if (c >= 3 && group_magic(S, c <= 8 ? 0 : 1)) return group_param(S, c);
+  if ((c == 1 || c == 2) && seg_m12(S)) {
+    // the magic-number format of c >= 3 (W <= 23: the binary32 value is exact)
+    const int W = seg_W(S, c);
+    FieldPar p;
+    if (W == 0) {
+      p.x = 0u;
+      p.y = kMagic;
+      p.z = 32u;
+      p.w = 0xCB000000u;
+    } else {
+      const int k = field_pair(c, seg_k2(S), seg_kA(S), seg_kB(S));
+      p.x = (uint32_t)(seg_o(S, c) - 32 * k);
+      p.y = kMagic >> W;
+      p.z = 32u - (uint32_t)W;
+      p.w = 0xCB000000u + (1u << (W - 1));
+    }
+    return p;
+  }
+  return field_param(S, c);
 }
 
 // the group bits at the bottom of a register

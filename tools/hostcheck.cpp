@@ -384,6 +384,12 @@ int64_t hc_unpack(const uint8_t* segs_in, const uint32_t* body, const uint64_t* 
               const int k = pk::field_pair(c, pk::seg_k2(S), pk::seg_kA(S), pk::seg_kB(S));
               same = same && pk::field_f(a[k], k + 1 < pk::kFastWords ? a[k + 1] : 0u, par[c]) == (float)q[c];
             }
+            // c = 1, 2 in the magic-number format (seg_m12) give the same q
+            if (pk::seg_m12(S))
+              for (int c = 1; c <= 2; ++c) {
+                const int k = pk::field_pair(c, pk::seg_k2(S), pk::seg_kA(S), pk::seg_kB(S));
+                same = same && pk::field_f(a[k], a[k + 1], pk::seg_param(S, c)) == (float)q[c];
+              }
             // the group path (k_pk_gemv2, groups of <= 23 bits) gives the same q
             for (int gg = 0; gg < 2; ++gg) {
               if (!pk::group_magic(S, gg)) continue;
