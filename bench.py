@@ -713,7 +713,7 @@ def b200_main(args, world, rank, local):
                 "ms_per_step": round(e2e_ms, 4), "h2d_bytes_per_step": T * 4,
                 "d2h_bytes_per_step": out_rows * 4},
         "gpu_launches": launches_per_step * args.steps,
-        "roofline": {"bound": "hbm", "kernel": "k_pk_gemv" if args.layout == "packed" else "k_decode_gemv",
+        "roofline": {"bound": "hbm", "kernel": "k_pk_gemv2" if args.layout == "packed" else "k_decode_gemv",
                      "bytes": ("tile-packed copy read by the launch (body + segment headers + "
                                "exception list) + vector + output" if args.layout == "packed" else
                                "WHFZ payload + device index + vector + output"),
