@@ -1,7 +1,10 @@
 """BASELINE configs[1]: mid-size synthetic compressed matrix (4,096 x 262,144,
 1.07 G values) -- one fused decode+GEMV per mode and evaluation on one B200,
 against the HBM roofline.  Prints one JSON line per case.
-Usage: python tools/sweep_config2.py [rows] [cols]"""
+Usage: python tools/sweep_config2.py [rows] [cols] [layout: packed | skeleton-first]
+
+roofline_frac: the launch's own bytes (packed copy, or payload + index) over
+the HBM peak; reference_stream_frac: the WHFZ stream bytes over the same time."""
 import json
 import os
 import sys
@@ -14,8 +17,12 @@ from paper_1902_08018_b200.executor import GemvPlan  # noqa: E402
 
 rows = int(sys.argv[1]) if len(sys.argv) > 1 else 4096
 cols = int(sys.argv[2]) if len(sys.argv) > 2 else 262144
-peak = json.load(open(os.path.join(os.path.dirname(os.path.dirname(os.path.abspath(__file__))),
-                                   "MEASURED_PEAKS.json")))["hbm_gbs"]
+layout = sys.argv[3] if len(sys.argv) > 3 else "packed"
+try:
+    peak = json.load(open(os.path.join(os.path.dirname(os.path.dirname(os.path.abspath(__file__))),
+                                       "MEASURED_PEAKS.json")))["hbm_gbs"]
+except OSError:
+    peak = 6650.0   # B200_PROFILING.md fallback
 spec = synth.Spec(grid_rows=608, grid_cols=608, S=cols, K=rows, M=378, seed=11)
 C = torch.empty((rows, cols), dtype=torch.float32, device="cuda")
 for r0 in range(0, rows, 512):                       # generated in row bands
@@ -27,7 +34,10 @@ modes = [codec.FixedRate(4), codec.FixedRate(8), codec.FixedRate(16), codec.Fixe
 words = torch.empty_like(C)
 for mode in modes:
     ds = codec.compress_device(C, mode)
-    ds.relayout("skeleton-first")
+    if layout == "packed":
+        ds.pack()
+    else:
+        ds.relayout(layout)
     # decode-only (codec.decompress on the device: bit-exact binary32 words to HBM)
     for _ in range(2):
         ds.decode(out=words, check=False)
@@ -67,8 +77,9 @@ for mode in modes:
             "evaluation": ev, "compressed_bytes": comp, "bpv": round(8 * comp / (rows * cols), 3),
             "ms": round(ms, 4), "compressed_gbs": round(comp / ms / 1e6, 1),
             "gflops": round(rows * (2 * cols - 1) / ms / 1e6, 1),
-            "decoded_gbs": round(4 * rows * cols / ms / 1e6, 1),
-            "roofline_frac": round((plan.bytes_read + plan.bytes_written) / ms / 1e6 / peak, 4)}),
+            "decoded_gbs": round(4 * rows * cols / ms / 1e6, 1), "layout": layout,
+            "roofline_frac": round((plan.bytes_read + plan.bytes_written) / ms / 1e6 / peak, 4),
+            "reference_stream_frac": round(comp / ms / 1e6 / peak, 4)}),
             flush=True)
         plan.close()
     ds.close()
