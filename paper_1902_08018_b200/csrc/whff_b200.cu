@@ -1497,9 +1497,12 @@ whff_status_t whff_dstream_clone(whff_dstream_t s, whff_dstream_t* out) {
       e = cudaMemcpy(c->d_pk_segs, s->d_pk_segs, pk_segs_bytes(nseg), cudaMemcpyDeviceToDevice);
     const uint64_t ne = std::max<uint64_t>(s->pk_nexc, 1);
     if (e == cudaSuccess) e = cudaMalloc(&c->d_pk_exc_block, ne * 8);
-    if (e == cudaSuccess) e = cudaMemcpy(c->d_pk_exc_block, s->d_pk_exc_block, ne * 8, cudaMemcpyDeviceToDevice);
+    // (the exception list has a placeholder entry when empty: copy the real ones)
+    if (e == cudaSuccess && s->pk_nexc)
+      e = cudaMemcpy(c->d_pk_exc_block, s->d_pk_exc_block, s->pk_nexc * 8, cudaMemcpyDeviceToDevice);
     if (e == cudaSuccess) e = cudaMalloc(&c->d_pk_exc_words, ne * 64);
-    if (e == cudaSuccess) e = cudaMemcpy(c->d_pk_exc_words, s->d_pk_exc_words, ne * 64, cudaMemcpyDeviceToDevice);
+    if (e == cudaSuccess && s->pk_nexc)
+      e = cudaMemcpy(c->d_pk_exc_words, s->d_pk_exc_words, s->pk_nexc * 64, cudaMemcpyDeviceToDevice);
   }
   if (e != cudaSuccess) { free_stream(c); return cuda_fail(e, "clone"); }
   *out = c;

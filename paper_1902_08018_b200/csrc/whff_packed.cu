@@ -3,6 +3,7 @@
 // staged, coefficient evaluation), the exact-evaluation GEMV (k_pk_exact),
 // decode-only words and the exception side list, and their host launchers
 // (whff_packed_api.h).  The packer is whff_pack.cu.
+#include <cstddef>
 #include <type_traits>
 
 #include "whff_common.cuh"
@@ -376,20 +377,55 @@ constexpr int kP2Warps = 4;                              // warps per CTA
 constexpr int kP2Split = kPkVW / kP2Warps;               // CTAs per band
 constexpr int kP2Stages = WHFF_P2_STAGES;
 constexpr int kP2ItemTiles = WHFF_P2_ITEM;               // tiles per stage
+#ifdef WHFF_P2_COMPACT
+static_assert(WHFF_P2_ITEM >= 2, "a compact stage holds a 5-word tile only in two tile slots");
+constexpr int kP2TileBytes = 128 * 4 * 4;                // stage tile slot: <= 4 record words
+#else
 constexpr int kP2TileBytes = 128 * pk::kFastWords * 4;   // fast path: <= 5 record words
+#endif
+// tiles per item for a segment of R record words (a 5-word tile needs a
+// whole compact stage)
+__device__ __forceinline__ int p2_item_tiles(int R) {
+  return 128 * 4 * R * 1 <= kP2TileBytes ? WHFF_P2_ITEM : 1;
+}
 constexpr int kP2UBytes = kP2ItemTiles * 32 * 16;        // the items' slice of U
 constexpr int kP2StageBytes = kP2ItemTiles * kP2TileBytes + kP2UBytes;
-constexpr int kP2HdrRing = 32;                           // segment headers held per warp
-constexpr int kP2HdrChunk = 16;
+constexpr int kP2HdrRing = 16;                           // segment headers held per warp
+constexpr int kP2HdrChunk = 8;
 
+// Per-warp state the tile loop does not touch lives in shared memory (read
+// and written through volatile accesses), so it holds no registers across
+// the decode: the job's pointers, the producer's cursor, the header ring fill.
+struct P2Ctl {
+  uint64_t body, U, gsegs, gpars, policy, pbody;   // pointers (and the L2 policy)
+  uint32_t pk, pt, pslot, pntl, ptw, pcol0;        // producer cursor
+  uint32_t nseg, hdr_loaded, vw, ntile;
+};
 template <typename AT>
 struct alignas(128) P2Warp {
   uint8_t stage[kP2Stages][kP2StageBytes];
   uint64_t bar[kP2Stages];
   pk::Seg seg[kP2HdrRing];
-  pk::FieldPar par[16];
+  pk::FieldPar par[2][16];     // this segment's and the next one's (cp.async prefetch)
   AT rs[16];
+  P2Ctl ctl;
 };
+__device__ __forceinline__ uint32_t ctl_ld32(uint32_t a) {
+  uint32_t v;
+  asm volatile("ld.shared.u32 %0, [%1];" : "=r"(v) : "r"(a));
+  return v;
+}
+__device__ __forceinline__ uint64_t ctl_ld64(uint32_t a) {
+  uint64_t v;
+  asm volatile("ld.shared.u64 %0, [%1];" : "=l"(v) : "r"(a));
+  return v;
+}
+__device__ __forceinline__ void ctl_st32(uint32_t a, uint32_t v) {
+  asm volatile("st.shared.u32 [%0], %1;" ::"r"(a), "r"(v) : "memory");
+}
+__device__ __forceinline__ void ctl_st64(uint32_t a, uint64_t v) {
+  asm volatile("st.shared.u64 [%0], %1;" ::"r"(a), "l"(v) : "memory");
+}
 
 __device__ __forceinline__ uint32_t smem_addr(const void* p) {
   return (uint32_t)__cvta_generic_to_shared(p);
@@ -610,13 +646,23 @@ __device__ __forceinline__ void p2_tile(uint32_t tw, uint32_t uw, uint32_t par, 
       else run(C9_(), C15_(), I2(), T_(), F_(), F_());
     }
   }
+  // s += w 2^k: the product is exact, one rounding per term (most segments
+  // have a single emax, W_e = 0: one scale for the whole tile)
+  if (We == 0) {
+    const float sc = __uint_as_float(ebase_bits);
 #pragma unroll
-  for (int h = 0; h < 2; ++h) {
-    const uint32_t ea = pk::field_edelta(a[2 * h][0], We), eb = pk::field_edelta(a[2 * h + 1][0], We);
-    const float2 sc = make_float2(__uint_as_float(ebase_bits + (ea << 23)), __uint_as_float(ebase_bits + (eb << 23)));
-    // s += w 2^k: the product is exact, one rounding per term
+    for (int h = 0; h < 2; ++h)
 #pragma unroll
-    for (int r = 0; r < 4; ++r) s[h][r] = __ffma2_rn(w[h][r], sc, s[h][r]);
+      for (int r = 0; r < 4; ++r) s[h][r] = __ffma2_rn(w[h][r], make_float2(sc, sc), s[h][r]);
+  } else {
+#pragma unroll
+    for (int h = 0; h < 2; ++h) {
+      const uint32_t ea = pk::field_edelta(a[2 * h][0], We), eb = pk::field_edelta(a[2 * h + 1][0], We);
+      const float2 sc =
+          make_float2(__uint_as_float(ebase_bits + (ea << 23)), __uint_as_float(ebase_bits + (eb << 23)));
+#pragma unroll
+      for (int r = 0; r < 4; ++r) s[h][r] = __ffma2_rn(w[h][r], sc, s[h][r]);
+    }
   }
 }
 
@@ -632,71 +678,112 @@ __global__ void __launch_bounds__(32 * kP2Warps, WHFF_P2_MINB) k_pk_gemv2(PkTabl
   P2Warp<AT>& W = reinterpret_cast<P2Warp<AT>*>(p2_smem)[warp];
   uint64_t first;
   const PkJob& J = pk_job(T, gband, first);
-  const PkView P = J.p;
-  const float* __restrict__ v = J.v;
-  const float4* __restrict__ U = J.U;
   const uint64_t band = J.band0 + (gband - first);
-  const int nrows = pk::band_rows(P.g, band);
-  const uint64_t bc = P.g.bc;
   const int vw = part * kP2Warps + warp;
-  const int nseg = P.g.nsegb > (uint64_t)vw ? (int)((P.g.nsegb - 1 - vw) / kVW + 1) : 0;
-  const pk::Seg* gsegs = P.segs + band * P.g.nsegb + vw;
-  const pk::FieldPar* gpars = P.pars + (band * P.g.nsegb + vw) * 16;
+
+  // shared-memory addresses (32-bit) of the warp's stages, barriers,
+  // parameters and control block
+  const uint32_t st0 = smem_addr(&W.stage[0][0]);
+  const uint32_t bar0 = smem_addr(&W.bar[0]);
+  const uint32_t par0 = smem_addr(&W.par[0][0]);
+  const uint32_t ctl = smem_addr(&W.ctl);
+  const uint32_t c_body = ctl + offsetof(P2Ctl, body), c_U = ctl + offsetof(P2Ctl, U);
+  const uint32_t c_gsegs = ctl + offsetof(P2Ctl, gsegs), c_gpars = ctl + offsetof(P2Ctl, gpars);
+  const uint32_t c_policy = ctl + offsetof(P2Ctl, policy), c_pbody = ctl + offsetof(P2Ctl, pbody);
+  const uint32_t c_pk = ctl + offsetof(P2Ctl, pk), c_pt = ctl + offsetof(P2Ctl, pt);
+  const uint32_t c_pslot = ctl + offsetof(P2Ctl, pslot), c_pntl = ctl + offsetof(P2Ctl, pntl);
+  const uint32_t c_ptw = ctl + offsetof(P2Ctl, ptw), c_pcol0 = ctl + offsetof(P2Ctl, pcol0);
+  const uint32_t c_nseg = ctl + offsetof(P2Ctl, nseg), c_hdr = ctl + offsetof(P2Ctl, hdr_loaded);
+  const uint32_t c_ntile = ctl + offsetof(P2Ctl, ntile);
+  {
+    const PkView& P = J.p;
+    const uint64_t nsegb = P.g.nsegb;
+    const int nseg = nsegb > (uint64_t)vw ? (int)((nsegb - 1 - vw) / kVW + 1) : 0;
+    if (lane == 0) {
+      uint64_t policy;
+      asm volatile("createpolicy.fractional.L2::evict_first.b64 %0, 1.0;" : "=l"(policy));
+      ctl_st64(c_body, reinterpret_cast<uint64_t>(P.body));
+      ctl_st64(c_U, reinterpret_cast<uint64_t>(J.U));
+      ctl_st64(c_gsegs, reinterpret_cast<uint64_t>(P.segs + band * nsegb + vw));
+      ctl_st64(c_gpars, reinterpret_cast<uint64_t>(P.pars + (band * nsegb + vw) * 16));
+      ctl_st64(c_policy, policy);
+      ctl_st32(c_pk, 0);
+      ctl_st32(c_pt, 0);
+      ctl_st32(c_pslot, 0);
+      ctl_st32(c_nseg, (uint32_t)nseg);
+      ctl_st32(c_hdr, 0);
+      ctl_st32(c_ntile, (uint32_t)P.g.ntile);
+    }
+    if (lane < 16) W.rs[lane] = (AT)0;
+    if (lane == 0) {
+#pragma unroll
+      for (int i = 0; i < kP2Stages; ++i) mbar_init(&W.bar[i], 1);
+      asm volatile("fence.mbarrier_init.release.cluster;" ::: "memory");
+    }
+    __syncwarp();
+  }
 
   // segment headers -> a shared-memory ring, kP2HdrChunk at a time (the
   // producer runs at most kP2Stages items -- so at most kP2Stages segments --
   // ahead of the consumer: a header is never overwritten while needed)
-  int hdr_loaded = 0;
+  static_assert(kP2HdrRing - kP2HdrChunk > kP2Stages, "header ring too small");
   auto ensure_hdr = [&](int k) {
-    while (k >= hdr_loaded) {
-      __syncwarp();
-      const int kk = hdr_loaded + lane;
+    int loaded = (int)ctl_ld32(c_hdr);
+    if (k < loaded) return;
+    const pk::Seg* gsegs = reinterpret_cast<const pk::Seg*>(ctl_ld64(c_gsegs));
+    const int nseg = (int)ctl_ld32(c_nseg);
+    while (k >= loaded) {
+      const int kk = loaded + lane;
       if (lane < kP2HdrChunk && kk < nseg) W.seg[kk & (kP2HdrRing - 1)] = gsegs[(uint64_t)kVW * kk];
-      hdr_loaded += kP2HdrChunk;
-      __syncwarp();
+      loaded += kP2HdrChunk;
     }
+    __syncwarp();
+    if (lane == 0) ctl_st32(c_hdr, (uint32_t)loaded);
+    __syncwarp();
   };
   auto hdr = [&](int k) -> const pk::Seg& { return W.seg[k & (kP2HdrRing - 1)]; };
-  if (lane < 16) W.rs[lane] = (AT)0;
-  if (lane == 0) {
-#pragma unroll
-    for (int i = 0; i < kP2Stages; ++i) mbar_init(&W.bar[i], 1);
-    asm volatile("fence.mbarrier_init.release.cluster;" ::: "memory");
-  }
-  ensure_hdr(0);
-  uint64_t policy;
-  asm volatile("createpolicy.fractional.L2::evict_first.b64 %0, 1.0;" : "=l"(policy));
-
-  // shared-memory addresses (32-bit) of the warp's stages, barriers, parameters
-  const uint32_t st0 = smem_addr(&W.stage[0][0]);
-  const uint32_t bar0 = smem_addr(&W.bar[0]);
-  const uint32_t par0 = smem_addr(&W.par[0]);
-
-  // producer: lane 0 issues; the cursor (segment pk, tile pt) is warp-uniform.
-  // Per segment: its body, tile size and first column; per item: offsets.
-  int pk = 0, pt = 0, pslot = 0, pntl = 0;
-  uint32_t ptw = 0;
-  const uint32_t* pbody = nullptr;
-  uint32_t pcol0 = 0;
-  auto skip = [&]() {
+  auto seg_ntl = [&](int k) -> int {   // tiles of the warp's segment k
+    const uint64_t ntile = ctl_ld32(c_ntile);
+    const uint64_t t0 = (vw + (uint64_t)kVW * k) * pk::kSegTiles;
+    return ntile - t0 < (uint64_t)pk::kSegTiles ? (int)(ntile - t0) : pk::kSegTiles;
+  };
+  // producer: the cursor is warp-uniform and lives in W.ctl; lane 0 issues.
+  // skip(): from (pk, pt) to the next tile of a fast segment (or the end)
+  auto skip = [&](int pk, int pt) {
+    const int nseg = (int)ctl_ld32(c_nseg);
     while (pk < nseg) {
       ensure_hdr(pk);
       const pk::Seg& S = hdr(pk);
-      pntl = pk::seg_tiles(P.g, vw + (uint64_t)kVW * pk);
-      if (!pk::seg_generic(S) && pt < pntl) {
-        ptw = (uint32_t)pk::tile_words(pk::seg_L(S));
-        pbody = P.body + S.body + (uint64_t)pt * ptw;
-        pcol0 = (uint32_t)(((vw + (uint64_t)kVW * pk) * pk::kSegTiles + pt) * pk::kTile);
+      const int ntl = seg_ntl(pk);
+      if (!pk::seg_generic(S) && pt < ntl) {
+        if (lane == 0) {
+          const uint32_t tw = (uint32_t)pk::tile_words(pk::seg_L(S));
+          ctl_st32(c_ptw, tw);
+          ctl_st32(c_pntl, (uint32_t)ntl);
+          ctl_st64(c_pbody, ctl_ld64(c_body) + 4 * (S.body + (uint64_t)pt * tw));
+          ctl_st32(c_pcol0, (uint32_t)(((vw + (uint64_t)kVW * pk) * pk::kSegTiles + pt) * pk::kTile));
+        }
         break;
       }
       ++pk;
       pt = 0;
     }
+    if (lane == 0) {
+      ctl_st32(c_pk, (uint32_t)pk);
+      ctl_st32(c_pt, (uint32_t)pt);
+    }
+    __syncwarp();
   };
   auto issue = [&]() {
-    if (pk >= nseg) return;
-    const int nt = pntl - pt < kP2ItemTiles ? pntl - pt : kP2ItemTiles;
+    const int pk = (int)ctl_ld32(c_pk);
+    if (pk >= (int)ctl_ld32(c_nseg)) return;
+    const int pt = (int)ctl_ld32(c_pt), pntl = (int)ctl_ld32(c_pntl);
+    const int it = p2_item_tiles((int)(ctl_ld32(c_ptw) >> 7));
+    const int nt = pntl - pt < it ? pntl - pt : it;
     if (lane == 0) {
+      const uint32_t pslot = ctl_ld32(c_pslot), ptw = ctl_ld32(c_ptw), pcol0 = ctl_ld32(c_pcol0);
+      const uint64_t pbody = ctl_ld64(c_pbody), policy = ctl_ld64(c_policy);
+      const uint64_t usrc = ctl_ld64(c_U) + (uint64_t)pcol0 * 16;
       const uint32_t st = st0 + pslot * kP2StageBytes, bar = bar0 + 8 * pslot;
       const uint32_t tb = (uint32_t)nt * ptw * 4, ub = (uint32_t)nt * (pk::kTile * 16);   // U is padded
       asm volatile("mbarrier.arrive.expect_tx.shared::cta.b64 _, [%0], %1;" ::"r"(bar), "r"(tb + ub) : "memory");
@@ -705,45 +792,46 @@ __global__ void __launch_bounds__(32 * kP2Warps, WHFF_P2_MINB) k_pk_gemv2(PkTabl
           ::"r"(st), "l"(pbody), "r"(tb), "r"(bar), "l"(policy) : "memory");
       asm volatile(
           "cp.async.bulk.shared::cluster.global.mbarrier::complete_tx::bytes.L2::cache_hint [%0], [%1], %2, [%3], %4;"
-          ::"r"(st + kP2ItemTiles * kP2TileBytes), "l"(U + pcol0), "r"(ub), "r"(bar), "l"(policy) : "memory");
+          ::"r"(st + kP2ItemTiles * kP2TileBytes), "l"(usrc), "r"(ub), "r"(bar), "l"(policy) : "memory");
+      ctl_st32(c_pslot, pslot + 1 == kP2Stages ? 0u : pslot + 1);
+      ctl_st64(c_pbody, pbody + (uint64_t)nt * ptw * 4);
+      ctl_st32(c_pcol0, pcol0 + nt * pk::kTile);
+      ctl_st32(c_pt, (uint32_t)(pt + nt));
     }
-    pslot = pslot + 1 == kP2Stages ? 0 : pslot + 1;
-    pt += nt;
-    if (pt < pntl) {
-      pbody += nt * ptw;
-      pcol0 += nt * pk::kTile;
-    } else {
-      ++pk;
-      pt = 0;
-      skip();
-    }
+    __syncwarp();
+    if (pt + nt >= pntl) skip(pk + 1, 0);
   };
-  skip();
+  skip(0, 0);
   for (int i = 0; i < kP2Stages; ++i) issue();
 
-  // the next fast segment's parameters, prefetched (lanes 0..15)
-  pk::FieldPar pnext{0u, 0u, 0u, 0u};
-  if (lane < 16 && nseg > 0) pnext = gpars[lane];
+  // parameters of the warp's segment k -> par[k & 1] (cp.async: no registers)
+  auto prefetch_par = [&](int k) {
+    if (lane < 16 && k < (int)ctl_ld32(c_nseg)) {
+      const pk::FieldPar* gp = reinterpret_cast<const pk::FieldPar*>(ctl_ld64(c_gpars));
+      asm volatile("cp.async.cg.shared.global [%0], [%1], 16;" ::"r"(par0 + 256 * (k & 1) + 16 * lane),
+                   "l"(gp + (uint64_t)kVW * 16 * k + lane) : "memory");
+    }
+    asm volatile("cp.async.commit_group;" ::: "memory");
+  };
+  prefetch_par(0);
 
   AT acc = (AT)0;          // row (lane >> 1): the warp's binary64 (single: binary32) sum
   int cslot = 0;
   uint32_t cphase = 0;
+  const int nseg = (int)ctl_ld32(c_nseg);
 
   for (int k = 0; k < nseg; ++k) {
-    const uint64_t sb = vw + (uint64_t)kVW * k;
     ensure_hdr(k);
     const pk::Seg& S = hdr(k);   // shared memory
     const int L = pk::seg_L(S);
     const int We = pk::seg_We(S);
-    const int ntl = pk::seg_tiles(P.g, sb);
+    const int ntl = seg_ntl(k);
     const uint32_t ebase_bits = ((uint32_t)pk::seg_emax_base(S) - 59u) << 23;   // binary32 2^(emax_base - 186)
-    // this segment's parameters -> shared memory; prefetch the next one's
+    // this segment's parameters have landed; start the next one's
+    asm volatile("cp.async.wait_group 0;" ::: "memory");
     __syncwarp();
-    if (lane < 16) {
-      W.par[lane] = pnext;
-      if (k + 1 < nseg) pnext = gpars[(uint64_t)kVW * 16 * (k + 1) + lane];
-    }
-    __syncwarp();
+    prefetch_par(k + 1);
+    const uint32_t par = par0 + 256 * (k & 1);
     // the segment's per-lane binary32 sums: s[h][r] = (block-row 2h, 2h + 1) x row r
     float2 s[2][4];
 #pragma unroll
@@ -760,7 +848,8 @@ __global__ void __launch_bounds__(32 * kP2Warps, WHFF_P2_MINB) k_pk_gemv2(PkTabl
       const uint32_t twb = (uint32_t)pk::tile_words(L) * 4;   // bytes per tile
       auto items = [&](auto SPECC) {
         constexpr int SPEC = decltype(SPECC)::value;
-        for (int tt = 0; tt < ntl; tt += kP2ItemTiles) {
+        const int itl = p2_item_tiles(pk::rec_words(L));
+        for (int tt = 0; tt < ntl; tt += itl) {
           const uint32_t bar = bar0 + 8 * cslot;
           asm volatile(
               "{\n"
@@ -770,10 +859,10 @@ __global__ void __launch_bounds__(32 * kP2Warps, WHFF_P2_MINB) k_pk_gemv2(PkTabl
               "@!p bra W2C_WAIT_%=;\n"
               "}\n" ::"r"(bar), "r"(cphase) : "memory");
           const uint32_t st = st0 + cslot * kP2StageBytes + 16 * lane;
-          const int nt = ntl - tt < kP2ItemTiles ? ntl - tt : kP2ItemTiles;
+          const int nt = ntl - tt < itl ? ntl - tt : itl;
 #pragma unroll 1
           for (int it = 0; it < nt; ++it) {
-              p2_tile<SPEC>(st + it * twb, st + kP2ItemTiles * kP2TileBytes + it * (pk::kTile * 16), par0, m12,
+              p2_tile<SPEC>(st + it * twb, st + kP2ItemTiles * kP2TileBytes + it * (pk::kTile * 16), par, m12,
                             k2, hasA, gA, kA, hasB, gB, kB, We, ebase_bits, s);
           }
           // every lane has consumed the stage: refill it with the item kP2Stages ahead
@@ -788,16 +877,18 @@ __global__ void __launch_bounds__(32 * kP2Warps, WHFF_P2_MINB) k_pk_gemv2(PkTabl
       else items(std::integral_constant<int, kSpecAny>());
     } else {
       // generic segment (not staged): per-lane sequential parse from global memory
+      const PkView& P = J.p;
       const uint64_t TW = pk::tile_words(L);
       const uint32_t* sbody = P.body + S.body;
+      const uint64_t sb = vw + (uint64_t)kVW * k;
       for (int tt = 0; tt < ntl; ++tt) {
         const uint64_t col = (sb * pk::kSegTiles + tt) * pk::kTile + lane;
-        if (col >= bc) continue;
-        const float4 u4 = ldg(U + col);
+        if (col >= P.g.bc) continue;
+        const float4 u4 = ldg(J.U + col);
         const float u[4] = {u4.x, u4.y, u4.z, u4.w};
 #pragma unroll
         for (int i = 0; i < 4; ++i) {
-          if (i >= nrows) break;
+          if (i >= pk::band_rows(P.g, band)) break;
           int32_t q[16];
           uint32_t ed;
           pk_generic_parse(&hdr(k), sbody + tt * TW, lane, i, q, &ed);
@@ -826,9 +917,11 @@ __global__ void __launch_bounds__(32 * kP2Warps, WHFF_P2_MINB) k_pk_gemv2(PkTabl
       d[m] = (AT)((i & 1) ? s[i >> 1][r].y : s[i >> 1][r].x);
     }
     acc = acc + warp_transpose_reduce<AT>(d, lane);
-    if (S.exc_count) pk_exceptions<POL, AT>(P, v, band, S.exc_begin, S.exc_count, lane, W.rs);
+    if (S.exc_count) pk_exceptions<POL, AT>(J.p, J.v, band, S.exc_begin, S.exc_count, lane, W.rs);
   }
-  pk_band_epilogue<WHFF_EVAL_COEFF, POL, AT>(T, J, P, gband, band, nrows, vw, lane, &acc, true, W.rs, status);
+  asm volatile("cp.async.wait_group 0;" ::: "memory");
+  pk_band_epilogue<WHFF_EVAL_COEFF, POL, AT>(T, J, J.p, gband, band, pk::band_rows(J.p.g, band), vw, lane, &acc, true,
+                                             W.rs, status);
 }
 
 template <int POL>
