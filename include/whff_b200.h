@@ -283,6 +283,10 @@ whff_status_t whff_gemv(const float* a_dev, uint64_t lda, uint64_t rows, uint64_
 /* binary64 ground truth (mpgemv.py:64-69 gemv_oracle): y64 = cumsum order */
 whff_status_t whff_gemv_oracle(const float* a_dev, uint64_t lda, uint64_t rows, uint64_t cols,
                                const float* v_dev, double* y_dev, whff_stream_t stream);
+/* The same on binary64 inputs (mpgemv.py:64-69 casts to float64 first:
+ * binary64 products, sequential sum).                                     */
+whff_status_t whff_gemv_oracle_f64(const double* A, uint64_t lda, uint64_t rows, uint64_t cols,
+                                   const double* v, double* y, whff_stream_t stream);
 
 /* First non-finite element (mpgemv.py:42-51, codec.py:231, thermal.py:91-95):
  * atomically lowers *status_dev to its flat index.                       */

@@ -75,6 +75,7 @@ _SIG = {
     "whff_gemv_workspace_size": ([_U64, _U64, _I, _I, _I, _P], _I),
     "whff_gemv": ([_P, _U64, _U64, _U64, _P, _P, _I, _I, _I, _P, ctypes.c_size_t, _P], _I),
     "whff_gemv_oracle": ([_P, _U64, _U64, _U64, _P, _P, _P], _I),
+    "whff_gemv_oracle_f64": ([_P, _U64, _U64, _U64, _P, _P, _P], _I),
     "whff_find_nonfinite": ([_P, _U64, _P, _P], _I),
     "whff_csr_matvec": ([_P, _P, _P, _U64, _P, _P, _P, _P, _P], _I),
     "whff_source_term": ([_P, _P, ctypes.c_float, _U64, _P, _P], _I),

@@ -667,11 +667,14 @@ __global__ void WHFF_GEMV_LB k_decode_gemv(JobTable T, unsigned long long* statu
     // release: the record is visible before the count (no full fence: a
     // gpu-scope __threadfence per warp also invalidated the SM's L1)
     unsigned old;
-    asm volatile("atom.release.gpu.global.inc.u32 %0, [%1], %2;"
+    asm volatile("atom.acq_rel.gpu.global.inc.u32 %0, [%1], %2;"
                  : "=r"(old) : "l"(T.tickets + blockIdx.x / kSplit), "r"(kVW - 1u) : "memory");
     last = old == kVW - 1u;
   }
   if (!__shfl_sync(0xFFFFFFFFu, last, 0)) return;
+  // lane 0's acquire covers the warp once the warp synchronises (the shuffle
+  // alone carries no memory ordering to lanes 1..31)
+  __syncwarp();
   asm volatile("fence.acq_rel.gpu;" ::: "memory");   // the other warps' records (read via L2)
   VwRec P;
   {
@@ -782,6 +785,18 @@ __global__ void k_gemv_seq(const float* A, uint64_t lda, uint64_t rows, uint64_t
     if (F64OUT) y64[i] = acc;
     else y[i] = __double2float_rn(acc);
   }
+}
+
+// mpgemv.gemv_oracle (mpgemv.py:64-69) on binary64 inputs: binary64
+// products, sequential binary64 sum (np.cumsum order); one thread per row.
+__global__ void k_gemv_oracle64(const double* A, uint64_t lda, uint64_t rows, uint64_t cols, const double* v,
+                                double* y) {
+  const uint64_t i = blockIdx.x * (uint64_t)blockDim.x + threadIdx.x;
+  if (i >= rows) return;
+  const double* row = A + i * lda;
+  double acc = 0.0;
+  for (uint64_t j = 0; j < cols; ++j) acc = __dadd_rn(acc, __dmul_rn(row[j], v[j]));
+  y[i] = acc;
 }
 
 // fixed-fanout tree (K:50-77): leaf level from products, groups summed
@@ -2406,6 +2421,15 @@ whff_status_t whff_gemv_oracle(const float* A, uint64_t lda, uint64_t rows, uint
   k_gemv_seq<WHFF_POLICY_DOUBLE, true><<<grid_for(rows, 64), 64, 0, (cudaStream_t)stream>>>(
       A, lda, rows, cols, v, nullptr, y);
   WCK_LAUNCH("gemv oracle");
+  return WHFF_OK;
+}
+
+whff_status_t whff_gemv_oracle_f64(const double* A, uint64_t lda, uint64_t rows, uint64_t cols,
+                                   const double* v, double* y, whff_stream_t stream) {
+  if (!A || !v || !y) return fail(WHFF_ERR_ARGUMENT, "null argument");
+  if (rows < 1 || cols < 1) return fail(WHFF_ERR_DIMENSION, "gemv operands must be nonempty");
+  k_gemv_oracle64<<<grid_for(rows, 64), 64, 0, (cudaStream_t)stream>>>(A, lda, rows, cols, v, y);
+  WCK_LAUNCH("gemv oracle f64");
   return WHFF_OK;
 }
 

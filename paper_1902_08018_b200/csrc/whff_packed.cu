@@ -396,10 +396,11 @@ constexpr int kP2HdrChunk = 8;
 // Per-warp state the tile loop does not touch lives in shared memory (read
 // and written through volatile accesses), so it holds no registers across
 // the decode: the job's pointers, the producer's cursor, the header ring fill.
-struct P2Ctl {
-  uint64_t body, U, gsegs, gpars, policy, pbody;   // pointers (and the L2 policy)
-  uint32_t pk, pt, pslot, pntl, ptw, pcol0;        // producer cursor
-  uint32_t nseg, hdr_loaded, vw, ntile;
+struct alignas(16) P2Ctl {
+  uint64_t pbody, usrc;                  // next item: body and U source addresses
+  uint32_t pk, pt, pntl, pslot;          // producer cursor: segment, tile, its tiles, stage
+  uint32_t ptw, nseg, hdr_loaded, ntile; // words per tile of segment pk; warp constants
+  uint64_t body, U, gsegs, gpars, policy, pad;
 };
 template <typename AT>
 struct alignas(128) P2Warp {
@@ -420,6 +421,16 @@ __device__ __forceinline__ uint64_t ctl_ld64(uint32_t a) {
   asm volatile("ld.shared.u64 %0, [%1];" : "=l"(v) : "r"(a));
   return v;
 }
+__device__ __forceinline__ uint4 ctl_ld128(uint32_t a) {
+  uint4 v;
+  asm volatile("ld.shared.v4.u32 {%0, %1, %2, %3}, [%4];" : "=r"(v.x), "=r"(v.y), "=r"(v.z), "=r"(v.w) : "r"(a));
+  return v;
+}
+__device__ __forceinline__ void ctl_st128(uint32_t a, uint4 v) {
+  asm volatile("st.shared.v4.u32 [%0], {%1, %2, %3, %4};" ::"r"(a), "r"(v.x), "r"(v.y), "r"(v.z), "r"(v.w)
+               : "memory");
+}
+__device__ __forceinline__ uint64_t u64_of(uint32_t lo, uint32_t hi) { return ((uint64_t)hi << 32) | lo; }
 __device__ __forceinline__ void ctl_st32(uint32_t a, uint32_t v) {
   asm volatile("st.shared.u32 [%0], %1;" ::"r"(a), "r"(v) : "memory");
 }
@@ -439,24 +450,29 @@ __device__ __forceinline__ pk::FieldPar lds_par_a(uint32_t a) {
   return r;
 }
 
-// the transpose reduction of 16 per-lane values over a warp: afterwards lane
-// l holds the sum over the 32 lanes of value (l >> 1) (in a fixed order: the
-// xor-16, 8, 4, 2, 1 butterfly restricted to the values each lane keeps)
+// The transpose reduction of a segment's 16 per-lane sums over the warp:
+// afterwards lane l holds the sum over the 32 lanes of row m = l >> 1 of the
+// band (m = 4 i + r).  The first stage (xor 16: block-rows 0, 1 against 2, 3)
+// adds binary32 row pairs with FADD2; the rest (xor 8, 4, 2, 1) in AT -- the
+// butterfly restricted to the values each lane keeps.
 template <typename AT>
-__device__ __forceinline__ AT warp_transpose_reduce(AT d[16], int lane) {
-  AT e[8];
+__device__ __forceinline__ AT seg_reduce(const float2 s[2][4], int lane) {
   const bool b4 = lane & 16, b3 = lane & 8, b2 = lane & 4, b1 = lane & 2;
+  AT d[8];   // m - 8 b4 = 4 i' + r (i' = row within the kept pair)
 #pragma unroll
-  for (int j = 0; j < 8; ++j) {
-    const AT send = b4 ? d[j] : d[8 + j];
-    const AT mine = b4 ? d[8 + j] : d[j];
-    e[j] = mine + __shfl_xor_sync(0xFFFFFFFFu, send, 16);
+  for (int r = 0; r < 4; ++r) {
+    const float2 send = b4 ? s[0][r] : s[1][r];
+    const float2 mine = b4 ? s[1][r] : s[0][r];
+    const float2 e = __fadd2_rn(mine, make_float2(__shfl_xor_sync(0xFFFFFFFFu, send.x, 16),
+                                                  __shfl_xor_sync(0xFFFFFFFFu, send.y, 16)));
+    d[r] = (AT)e.x;
+    d[4 + r] = (AT)e.y;
   }
   AT f[4];
 #pragma unroll
   for (int j = 0; j < 4; ++j) {
-    const AT send = b3 ? e[j] : e[4 + j];
-    const AT mine = b3 ? e[4 + j] : e[j];
+    const AT send = b3 ? d[j] : d[4 + j];
+    const AT mine = b3 ? d[4 + j] : d[j];
     f[j] = mine + __shfl_xor_sync(0xFFFFFFFFu, send, 8);
   }
   AT g[2];
@@ -689,10 +705,10 @@ __global__ void __launch_bounds__(32 * kP2Warps, WHFF_P2_MINB) k_pk_gemv2(PkTabl
   const uint32_t ctl = smem_addr(&W.ctl);
   const uint32_t c_body = ctl + offsetof(P2Ctl, body), c_U = ctl + offsetof(P2Ctl, U);
   const uint32_t c_gsegs = ctl + offsetof(P2Ctl, gsegs), c_gpars = ctl + offsetof(P2Ctl, gpars);
-  const uint32_t c_policy = ctl + offsetof(P2Ctl, policy), c_pbody = ctl + offsetof(P2Ctl, pbody);
+  const uint32_t c_policy = ctl + offsetof(P2Ctl, policy), c_A = ctl + offsetof(P2Ctl, pbody);
+  const uint32_t c_B = ctl + offsetof(P2Ctl, pk), c_C = ctl + offsetof(P2Ctl, ptw);
   const uint32_t c_pk = ctl + offsetof(P2Ctl, pk), c_pt = ctl + offsetof(P2Ctl, pt);
   const uint32_t c_pslot = ctl + offsetof(P2Ctl, pslot), c_pntl = ctl + offsetof(P2Ctl, pntl);
-  const uint32_t c_ptw = ctl + offsetof(P2Ctl, ptw), c_pcol0 = ctl + offsetof(P2Ctl, pcol0);
   const uint32_t c_nseg = ctl + offsetof(P2Ctl, nseg), c_hdr = ctl + offsetof(P2Ctl, hdr_loaded);
   const uint32_t c_ntile = ctl + offsetof(P2Ctl, ntile);
   {
@@ -758,10 +774,13 @@ __global__ void __launch_bounds__(32 * kP2Warps, WHFF_P2_MINB) k_pk_gemv2(PkTabl
       if (!pk::seg_generic(S) && pt < ntl) {
         if (lane == 0) {
           const uint32_t tw = (uint32_t)pk::tile_words(pk::seg_L(S));
-          ctl_st32(c_ptw, tw);
+          const uint64_t col0 = ((vw + (uint64_t)kVW * pk) * pk::kSegTiles + pt) * pk::kTile;
+          const uint64_t pbody = ctl_ld64(c_body) + 4 * (S.body + (uint64_t)pt * tw);
+          const uint64_t usrc = ctl_ld64(c_U) + col0 * 16;
+          ctl_st128(c_A, make_uint4((uint32_t)pbody, (uint32_t)(pbody >> 32), (uint32_t)usrc,
+                                    (uint32_t)(usrc >> 32)));
+          ctl_st32(c_C, tw);
           ctl_st32(c_pntl, (uint32_t)ntl);
-          ctl_st64(c_pbody, ctl_ld64(c_body) + 4 * (S.body + (uint64_t)pt * tw));
-          ctl_st32(c_pcol0, (uint32_t)(((vw + (uint64_t)kVW * pk) * pk::kSegTiles + pt) * pk::kTile));
         }
         break;
       }
@@ -775,15 +794,18 @@ __global__ void __launch_bounds__(32 * kP2Warps, WHFF_P2_MINB) k_pk_gemv2(PkTabl
     __syncwarp();
   };
   auto issue = [&]() {
-    const int pk = (int)ctl_ld32(c_pk);
-    if (pk >= (int)ctl_ld32(c_nseg)) return;
-    const int pt = (int)ctl_ld32(c_pt), pntl = (int)ctl_ld32(c_pntl);
-    const int it = p2_item_tiles((int)(ctl_ld32(c_ptw) >> 7));
+    const uint4 B = ctl_ld128(c_B);   // pk, pt, pntl, pslot
+    const uint4 C = ctl_ld128(c_C);   // ptw, nseg, -, -
+    const int pk = (int)B.x;
+    if (pk >= (int)C.y) return;
+    const int pt = (int)B.y, pntl = (int)B.z;
+    const uint32_t ptw = C.x;
+    const int it = p2_item_tiles((int)(ptw >> 7));
     const int nt = pntl - pt < it ? pntl - pt : it;
     if (lane == 0) {
-      const uint32_t pslot = ctl_ld32(c_pslot), ptw = ctl_ld32(c_ptw), pcol0 = ctl_ld32(c_pcol0);
-      const uint64_t pbody = ctl_ld64(c_pbody), policy = ctl_ld64(c_policy);
-      const uint64_t usrc = ctl_ld64(c_U) + (uint64_t)pcol0 * 16;
+      const uint4 A = ctl_ld128(c_A);
+      const uint64_t pbody = u64_of(A.x, A.y), usrc = u64_of(A.z, A.w), policy = ctl_ld64(c_policy);
+      const uint32_t pslot = B.w;
       const uint32_t st = st0 + pslot * kP2StageBytes, bar = bar0 + 8 * pslot;
       const uint32_t tb = (uint32_t)nt * ptw * 4, ub = (uint32_t)nt * (pk::kTile * 16);   // U is padded
       asm volatile("mbarrier.arrive.expect_tx.shared::cta.b64 _, [%0], %1;" ::"r"(bar), "r"(tb + ub) : "memory");
@@ -793,10 +815,9 @@ __global__ void __launch_bounds__(32 * kP2Warps, WHFF_P2_MINB) k_pk_gemv2(PkTabl
       asm volatile(
           "cp.async.bulk.shared::cluster.global.mbarrier::complete_tx::bytes.L2::cache_hint [%0], [%1], %2, [%3], %4;"
           ::"r"(st + kP2ItemTiles * kP2TileBytes), "l"(usrc), "r"(ub), "r"(bar), "l"(policy) : "memory");
-      ctl_st32(c_pslot, pslot + 1 == kP2Stages ? 0u : pslot + 1);
-      ctl_st64(c_pbody, pbody + (uint64_t)nt * ptw * 4);
-      ctl_st32(c_pcol0, pcol0 + nt * pk::kTile);
-      ctl_st32(c_pt, (uint32_t)(pt + nt));
+      const uint64_t nb = pbody + tb, nu = usrc + ub;
+      ctl_st128(c_A, make_uint4((uint32_t)nb, (uint32_t)(nb >> 32), (uint32_t)nu, (uint32_t)(nu >> 32)));
+      ctl_st128(c_B, make_uint4(B.x, (uint32_t)(pt + nt), B.z, pslot + 1 == kP2Stages ? 0u : pslot + 1));
     }
     __syncwarp();
     if (pt + nt >= pntl) skip(pk + 1, 0);
@@ -910,13 +931,7 @@ __global__ void __launch_bounds__(32 * kP2Warps, WHFF_P2_MINB) k_pk_gemv2(PkTabl
       }
     }
     // the segment's sums over the warp (row m of the band: m = 4 i + r)
-    AT d[16];
-#pragma unroll
-    for (int m = 0; m < 16; ++m) {
-      const int i = m >> 2, r = m & 3;
-      d[m] = (AT)((i & 1) ? s[i >> 1][r].y : s[i >> 1][r].x);
-    }
-    acc = acc + warp_transpose_reduce<AT>(d, lane);
+    acc = acc + seg_reduce<AT>(s, lane);
     if (S.exc_count) pk_exceptions<POL, AT>(J.p, J.v, band, S.exc_begin, S.exc_count, lane, W.rs);
   }
   asm volatile("cp.async.wait_group 0;" ::: "memory");

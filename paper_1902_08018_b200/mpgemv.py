@@ -102,8 +102,23 @@ def gemv(req, backend=None):
 
 
 def gemv_oracle(matrix, vector):
-    """Binary64 ground truth, sequential order (mpgemv.py:64-69), on device."""
+    """Binary64 ground truth, sequential order (mpgemv.py:64-69), on device.
+    Binary64 inputs stay binary64 (the reference casts to float64 first)."""
     torch = _lib.require_cuda()
+    if _is_f64(matrix) or _is_f64(vector):
+        m = _to_device_f64(matrix, 2)
+        v = _to_device_f64(vector, 1)
+        if m.shape[1] != v.shape[0] or m.shape[0] < 1 or m.shape[1] < 1:
+            raise DimensionError(
+                f"gemv shapes do not agree: matrix {tuple(m.shape)}, vector {tuple(v.shape)}")
+        if not bool(torch.isfinite(m).all()):
+            raise NonFiniteError("matrix", int(torch.nonzero(~torch.isfinite(m.reshape(-1)))[0]))
+        if not bool(torch.isfinite(v).all()):
+            raise NonFiniteError("vector", int(torch.nonzero(~torch.isfinite(v))[0]))
+        out = torch.empty(m.shape[0], dtype=torch.float64, device=m.device)
+        _lib.call("whff_gemv_oracle_f64", _lib.ptr(m), m.stride(0), m.shape[0], m.shape[1], _lib.ptr(v),
+                  _lib.ptr(out), _lib.cur_stream())
+        return out.cpu().numpy()
     m = _to_device(matrix, 2)
     v = _to_device(vector, 1)
     _check_inputs(m, v)
@@ -111,6 +126,25 @@ def gemv_oracle(matrix, vector):
     _lib.call("whff_gemv_oracle", _lib.ptr(m), m.stride(0), m.shape[0], m.shape[1], _lib.ptr(v),
               _lib.ptr(out), _lib.cur_stream())
     return out.cpu().numpy()
+
+
+def _is_f64(x):
+    torch = _lib.require_cuda()
+    if isinstance(x, torch.Tensor):
+        return x.dtype == torch.float64
+    return np.asarray(x).dtype == np.float64
+
+
+def _to_device_f64(x, ndim):
+    torch = _lib.require_cuda()
+    if isinstance(x, torch.Tensor):
+        t = x.to(device="cuda", dtype=torch.float64)
+    else:
+        a = np.asarray(x, dtype=np.float64)
+        if a.ndim != ndim:
+            raise DimensionError(f"expected a {ndim}-D array, got shape {a.shape}")
+        t = torch.from_numpy(np.ascontiguousarray(a)).cuda()
+    return t.contiguous()
 
 
 def gemv_compressed(stream, vector, policy="mixed", evaluation="exact", row_begin=0,

@@ -28,10 +28,10 @@ import numpy as np
 KVW = 32
 
 
-def _butterfly(a):
+def _butterfly(a, offsets=(16, 8, 4, 2, 1)):
     """a: (..., 32) -> the xor-butterfly sum (identical in every lane), lane 0."""
     idx = np.arange(32)
-    for o in (16, 8, 4, 2, 1):
+    for o in offsets:
         a = a + a[..., idx ^ o]
     return a[..., 0]
 
@@ -327,8 +327,10 @@ def packed_model(orc, stream, v, policy="mixed", evaluation="coefficient"):
                                     D[vw, :, i, r] = np.where(m, D[vw, :, i, r] + Pa[b, cs, r, j],
                                                               D[vw, :, i, r])
                 if staged:
-                    Dseg = Sg.reshape(32, 16).astype(acc_t)          # [lane, m = 4 i + r]
-                    Dv_acc[vw] = Dv_acc[vw] + _butterfly(np.moveaxis(Dseg, 0, -1))
+                    # seg_reduce: xor-16 stage in binary32, then xor 8, 4, 2, 1
+                    Dseg = Sg.reshape(32, 16)                          # [lane, m = 4 i + r]
+                    X1 = (Dseg + Dseg[np.arange(32) ^ 16]).astype(np.float32).astype(acc_t)
+                    Dv_acc[vw] = Dv_acc[vw] + _butterfly(np.moveaxis(X1, 0, -1), (8, 4, 2, 1))
                 for tt in range(8):
                     for i in range(4):
                         b = 4 * band + i

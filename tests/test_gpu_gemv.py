@@ -95,3 +95,14 @@ def test_find_nonfinite_first_index_any_alignment():
         for i in idx:
             y[i] = random.choice([float("nan"), float("inf"), float("-inf")])
         assert find_nonfinite(y) == (idx[0] if idx else None)
+
+
+def test_gemv_oracle_keeps_binary64_inputs(rng):
+    """mpgemv.py:64-69 casts to float64: binary64 inputs (even beyond the
+    binary32 range) give the reference's np.cumsum result bit for bit."""
+    from paper_1902_08018_b200.mpgemv import gemv_oracle
+    m = rng.standard_normal((9, 1031)) * 1e200
+    v = rng.standard_normal(1031) * 1e-100
+    want = np.cumsum(m * v, axis=1, dtype=np.float64)[:, -1]
+    got = gemv_oracle(m, v)
+    assert got.dtype == np.float64 and np.array_equal(got, want)
