@@ -802,19 +802,24 @@ __global__ void __launch_bounds__(32 * kP2Warps, WHFF_P2_MINB) k_pk_gemv2(PkTabl
     const uint32_t ptw = C.x;
     const int it = p2_item_tiles((int)(ptw >> 7));
     const int nt = pntl - pt < it ? pntl - pt : it;
+    // the whole (converged) warp runs this with warp-uniform operands; one
+    // elected lane arms the barrier and issues the copies (no per-lane loop)
+    const uint4 A = ctl_ld128(c_A);
+    const uint64_t pbody = u64_of(A.x, A.y), usrc = u64_of(A.z, A.w), policy = ctl_ld64(c_policy);
+    const uint32_t pslot = B.w;
+    const uint32_t st = st0 + pslot * kP2StageBytes, bar = bar0 + 8 * pslot;
+    const uint32_t tb = (uint32_t)nt * ptw * 4, ub = (uint32_t)nt * (pk::kTile * 16);   // U is padded
+    asm volatile(
+        "{\n"
+        ".reg .pred p;\n"
+        "elect.sync _|p, 0xffffffff;\n"
+        "@p mbarrier.arrive.expect_tx.shared::cta.b64 _, [%1], %6;\n"
+        "@p cp.async.bulk.shared::cluster.global.mbarrier::complete_tx::bytes.L2::cache_hint [%0], [%2], %4, [%1], %7;\n"
+        "@p cp.async.bulk.shared::cluster.global.mbarrier::complete_tx::bytes.L2::cache_hint [%8], [%3], %5, [%1], %7;\n"
+        "}\n" ::"r"(st), "r"(bar), "l"(pbody), "l"(usrc), "r"(tb), "r"(ub), "r"(tb + ub), "l"(policy),
+        "r"(st + kP2ItemTiles * kP2TileBytes)
+        : "memory");
     if (lane == 0) {
-      const uint4 A = ctl_ld128(c_A);
-      const uint64_t pbody = u64_of(A.x, A.y), usrc = u64_of(A.z, A.w), policy = ctl_ld64(c_policy);
-      const uint32_t pslot = B.w;
-      const uint32_t st = st0 + pslot * kP2StageBytes, bar = bar0 + 8 * pslot;
-      const uint32_t tb = (uint32_t)nt * ptw * 4, ub = (uint32_t)nt * (pk::kTile * 16);   // U is padded
-      asm volatile("mbarrier.arrive.expect_tx.shared::cta.b64 _, [%0], %1;" ::"r"(bar), "r"(tb + ub) : "memory");
-      asm volatile(
-          "cp.async.bulk.shared::cluster.global.mbarrier::complete_tx::bytes.L2::cache_hint [%0], [%1], %2, [%3], %4;"
-          ::"r"(st), "l"(pbody), "r"(tb), "r"(bar), "l"(policy) : "memory");
-      asm volatile(
-          "cp.async.bulk.shared::cluster.global.mbarrier::complete_tx::bytes.L2::cache_hint [%0], [%1], %2, [%3], %4;"
-          ::"r"(st + kP2ItemTiles * kP2TileBytes), "l"(usrc), "r"(ub), "r"(bar), "l"(policy) : "memory");
       const uint64_t nb = pbody + tb, nu = usrc + ub;
       ctl_st128(c_A, make_uint4((uint32_t)nb, (uint32_t)(nb >> 32), (uint32_t)nu, (uint32_t)(nu >> 32)));
       ctl_st128(c_B, make_uint4(B.x, (uint32_t)(pt + nt), B.z, pslot + 1 == kP2Stages ? 0u : pslot + 1));
