@@ -684,7 +684,7 @@ def b200_main(args, world, rank, local):
                              "budget_at_hbm_peak": round(budget, 1),
                              "alu_pipe_pct": e.get("alu_pipe_pct"),
                              "issue_active_pct": e.get("issue_active_pct"),
-                             "source": "ncu --set full (profiles/r1_ncu_summary.md)"}
+                             "source": "ncu --set full (profiles/r2_ncu_summary.md, profiles/ncu_traffic.json)"}
     except Exception:
         pass
     p50 = statistics.median(lat_ms)

@@ -819,6 +819,7 @@ __global__ void __launch_bounds__(32 * kP2Warps, WHFF_P2_MINB) k_pk_gemv2(PkTabl
         "}\n" ::"r"(st), "r"(bar), "l"(pbody), "l"(usrc), "r"(tb), "r"(ub), "r"(tb + ub), "l"(policy),
         "r"(st + kP2ItemTiles * kP2TileBytes)
         : "memory");
+    __syncwarp();   // every lane has read the cursor before lane 0 advances it
     if (lane == 0) {
       const uint64_t nb = pbody + tb, nu = usrc + ub;
       ctl_st128(c_A, make_uint4((uint32_t)nb, (uint32_t)(nb >> 32), (uint32_t)nu, (uint32_t)(nu >> 32)));
