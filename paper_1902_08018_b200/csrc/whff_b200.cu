@@ -761,6 +761,14 @@ __global__ void k_coeff_prep(const float* v, uint64_t cols, uint64_t bc, uint64_
   U[b] = make_float4(u[0], u[1], u[2], u[3]);
 }
 
+// v per block-column as float4, zero-padded past cols and to whole 32-column
+// tiles (the staged exact evaluation copies it in tile slices like U)
+__global__ void k_vpad(const float* v, uint64_t cols, uint64_t bc, uint64_t bcp, float4* V) {
+  const uint64_t b = blockIdx.x * (uint64_t)blockDim.x + threadIdx.x;
+  if (b >= bcp) return;
+  V[b] = b < bc ? load_v4(v, b, cols, false) : make_float4(0.f, 0.f, 0.f, 0.f);
+}
+
 // ---------------------------------------------------------------------------
 // Dense GEMV policies (K:24-132)
 // ---------------------------------------------------------------------------
@@ -1102,6 +1110,16 @@ __global__ void k_build_compact(const uint64_t* offsets, uint64_t nb, uint64_t b
 namespace {
 
 inline unsigned grid_for(uint64_t n, unsigned t) { return (unsigned)((n + t - 1) / t); }
+
+// the per-launch vector prologue: U = G^T v (coefficient) or padded v (exact
+// evaluation of a packed stream)
+static void vec_prologue(int eval, const float* v, uint64_t cols, uint64_t bc, float4* out, cudaStream_t cs) {
+  if (eval == WHFF_EVAL_COEFF)
+    k_coeff_prep<<<grid_for(pad_tiles(bc), 256), 256, 0, cs>>>(v, cols, bc, pad_tiles(bc), out);
+  else
+    k_vpad<<<grid_for(pad_tiles(bc), 256), 256, 0, cs>>>(v, cols, bc, pad_tiles(bc), out);
+}
+
 
 struct DeviceGuard {
   int prev = -1;
@@ -1943,7 +1961,7 @@ static whff_status_t launch_gemv(int var, int eval, bool sf, const JobTable& T, 
 // [per-row virtual-warp partials][per-row arrival counters]
 static uint64_t align256(uint64_t x) { return (x + 255) & ~255ull; }
 static uint64_t ws_u_bytes(const whff_dstream* s, int eval) {
-  return eval == WHFF_EVAL_COEFF ? align256(pad_tiles(s->bc) * sizeof(float4)) : 0;
+  return (eval == WHFF_EVAL_COEFF || s->packed) ? align256(pad_tiles(s->bc) * sizeof(float4)) : 0;
 }
 static uint64_t ws_rec_bytes(const whff_dstream* s) {
   return align256(std::max<uint64_t>(s->br, 1) * kVW * sizeof(VwRec));
@@ -2010,12 +2028,9 @@ extern "C" whff_status_t whff_decode_gemv(whff_dstream_t s, const float* v, floa
     T.tickets = reinterpret_cast<unsigned*>(wsb + ws_u_bytes(s, eval) + ws_pkrec_bytes(s));
     cudaError_t me = cudaMemsetAsync(T.tickets, 0, T.total_bands * sizeof(unsigned), cs);
     if (me != cudaSuccess) return cuda_fail(me, "workspace clear");
-    if (eval == WHFF_EVAL_COEFF) {
-      k_coeff_prep<<<grid_for(pad_tiles(s->bc), 256), 256, 0, cs>>>(v, s->cols, s->bc, pad_tiles(s->bc),
-                                                                 reinterpret_cast<float4*>(ws));
-      WCK_LAUNCH("coeff_prep");
-      T.single.U = reinterpret_cast<const float4*>(ws);
-    }
+    vec_prologue(eval, v, s->cols, s->bc, reinterpret_cast<float4*>(ws), cs);
+    WCK_LAUNCH("vector prologue");
+    T.single.U = reinterpret_cast<const float4*>(ws);
     return launch_pk(eval, policy, T, reinterpret_cast<unsigned long long*>(status), cs);
   }
   JobTable T;
@@ -2131,7 +2146,7 @@ static whff_status_t plan_create_packed(int n, const whff_dstream_t* streams, co
   plan_vectors(P, n, streams, v, uoff, ucount);
   P->total_warps = bands;
   cudaError_t e = cudaSuccess;
-  if (eval == WHFF_EVAL_COEFF) {
+  {   // U = G^T v (coefficient) or padded v (exact) per distinct vector
     e = cudaMalloc(&P->d_U, std::max<uint64_t>(ucount, 1) * sizeof(float4));
     for (int i = 0; i < n && e == cudaSuccess; ++i) jobs[i].U = P->d_U + uoff[i];
   }
@@ -2264,12 +2279,10 @@ whff_status_t whff_gemv_plan_launch(whff_gemv_plan_t P, uint64_t* status, whff_s
   if (!P || !status) return fail(WHFF_ERR_ARGUMENT, "null argument");
   DeviceGuard g(P->device);
   cudaStream_t cs = (cudaStream_t)stream;
-  if (P->eval == WHFF_EVAL_COEFF) {
-    for (size_t k = 0; k < P->prep_v.size(); ++k) {
-      k_coeff_prep<<<grid_for(pad_tiles(P->prep_bc[k]), 256), 256, 0, cs>>>(
-          P->prep_v[k], P->prep_cols[k], P->prep_bc[k], pad_tiles(P->prep_bc[k]), P->d_U + P->prep_off[k]);
-    }
-    WCK_LAUNCH("plan coeff_prep");
+  if (P->eval == WHFF_EVAL_COEFF || P->pk) {
+    for (size_t k = 0; k < P->prep_v.size(); ++k)
+      vec_prologue(P->eval, P->prep_v[k], P->prep_cols[k], P->prep_bc[k], P->d_U + P->prep_off[k], cs);
+    WCK_LAUNCH("plan vector prologue");
   }
   if (P->pk) {
     PkTable T;

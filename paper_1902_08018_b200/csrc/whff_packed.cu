@@ -1,8 +1,9 @@
 // whff_packed.cu -- kernels of the tile-packed layout (whff_packed.cuh):
-// the fused decode + GEMV that reads it (the hot path: k_pk_gemv2, TMA-
-// staged, coefficient evaluation), the exact-evaluation GEMV (k_pk_exact),
-// decode-only words and the exception side list, and their host launchers
-// (whff_packed_api.h).  The packer is whff_pack.cu.
+// the fused decode + GEMV that reads it (k_pk_gemv2, TMA-staged: the
+// coefficient evaluation -- the hot path -- and the exact evaluation with the
+// reference's binary32 products), decode-only words and the exception side
+// list, and their host launchers (whff_packed_api.h).  The packer is
+// whff_pack.cu.
 #include <cstddef>
 #include <type_traits>
 
@@ -240,107 +241,10 @@ __device__ __forceinline__ void pk_band_epilogue(const PkTable& T, const PkJob& 
 }
 
 // ---------------------------------------------------------------------------
-// fused decode + GEMV, exact evaluation: the reference's binary32 words x v
+// fused decode + GEMV, TMA-staged (the hot path)
 // ---------------------------------------------------------------------------
-// Four CTAs of 8 warps per band; virtual warp vw (of kVW) takes segments
-// vw, vw + 32, ...; lane l the block-column 32 t + l of every tile t; per lane
-// binary64 (mixed, double) or binary32 (single) sums per (block-row, row) in
-// tile, row and column order; words are reconstructed bit-exactly
-// (codec.py:128-218) from the packed coefficients.
-template <int POL>
-__global__ void __launch_bounds__(32 * kPkWarps, 2) k_pk_exact(PkTable T, unsigned long long* status) {
-  using A = PkAcc<POL>;
-  using AT = typename A::T;
-  const uint64_t gband = blockIdx.x / kPkSplit;
-  const int part = (int)(blockIdx.x % kPkSplit);
-  if (gband >= T.total_bands) return;
-  const int lane = threadIdx.x & 31;
-  const int warp = threadIdx.x >> 5;
-  uint64_t first;
-  const PkJob& J = pk_job(T, gband, first);
-  const PkView P = J.p;
-  const float* __restrict__ v = J.v;
-  const uint64_t band = J.band0 + (gband - first);
-  const int nrows = pk::band_rows(P.g, band);
-  const uint64_t bc = P.g.bc;
-  const bool v_aligned = ((reinterpret_cast<uintptr_t>(v) & 15u) == 0);
-  const uint32_t last_colmask = (P.g.cols & 3) ? ((1u << (P.g.cols & 3)) - 1u) : 0xFu;
-
-  __shared__ pk::FieldPar s_par[kPkWarps][16];
-  __shared__ AT s_rs[kPkWarps][16];
-  __shared__ pk::Seg s_seg[kPkWarps];
-  pk::FieldPar* par = s_par[warp];
-  AT* rs = s_rs[warp];
-  if (lane < 16) rs[lane] = (AT)0;
-  A acc;
-#pragma unroll
-  for (int i = 0; i < 4; ++i)
-#pragma unroll
-    for (int r = 0; r < 4; ++r) acc.v[i][r] = (AT)0;
-
-  const int vw = part * kPkWarps + warp;
-  for (uint64_t sb = vw; sb < P.g.nsegb; sb += kVW) {
-    const pk::Seg S = P.segs[band * P.g.nsegb + sb];
-    const int L = pk::seg_L(S), R = pk::rec_words(L);
-    const int We = pk::seg_We(S);
-    const uint64_t TW = pk::tile_words(L);
-    const int ntl = pk::seg_tiles(P.g, sb);
-    const uint32_t ebase = (uint32_t)pk::seg_emax_base(S);
-    const uint32_t* sbody = P.body + S.body;
-    const bool generic = pk::seg_generic(S);
-    __syncwarp();
-    if (!generic && lane < 16) par[lane] = pk::field_param(S, lane);
-    if (lane == 0) s_seg[warp] = S;
-    __syncwarp();
-    const bool k2 = pk::seg_k2(S), kA = pk::seg_kA(S), kB = pk::seg_kB(S);
-    for (int tt = 0; tt < ntl; ++tt) {
-      const uint64_t col = (sb * pk::kSegTiles + tt) * pk::kTile + lane;
-      if (col >= bc) continue;
-      const uint32_t* tile = sbody + tt * TW;
-      const float4 v4 = load_v4(v, col, P.g.cols, v_aligned);
-      const float vv[4] = {v4.x, v4.y, v4.z, v4.w};
-      const uint32_t colmask = (col + 1 == bc) ? last_colmask : 0xFu;
-#pragma unroll
-      for (int i = 0; i < 4; ++i) {
-        if (i >= nrows) break;
-        int32_t q[16];
-        uint32_t ed;
-        if (!generic) {
-          uint32_t a[pk::kFastWords];
-          pk_rec_fast(a, tile, R, lane, i);
-          pk_fields_int(a, par, k2, kA, kB, q);
-          ed = pk::field_edelta(a[0], We);
-        } else {
-          pk_generic_parse(&s_seg[warp], tile, lane, i, q, &ed);
-        }
-        float x[16];
-        pk::words_from_q(q, ebase + ed, x);
-#pragma unroll
-        for (int kk = 0; kk < 16; ++kk)
-          if (!((colmask >> (kk & 3)) & 1u)) x[kk] = 0.0f;
-        pk_acc_words<POL>(acc.v[i], x, vv);
-      }
-    }
-    if (S.exc_count) pk_exceptions<POL, AT>(P, v, band, S.exc_begin, S.exc_count, lane, rs);
-  }
-
-  // warp butterfly over the 16 rows, then the band's epilogue
-#pragma unroll
-  for (int o = 16; o > 0; o >>= 1)
-#pragma unroll
-    for (int i = 0; i < 4; ++i)
-#pragma unroll
-      for (int r = 0; r < 4; ++r) acc.v[i][r] = acc.v[i][r] + __shfl_xor_sync(0xFFFFFFFFu, acc.v[i][r], o);
-  __syncwarp();
-  pk_band_epilogue<WHFF_EVAL_EXACT, POL, AT>(T, J, P, gband, band, nrows, vw, lane, &acc.v[0][0], false, rs,
-                                             status);
-}
-
-// ---------------------------------------------------------------------------
-// fused decode + GEMV, coefficient evaluation, TMA-staged (the hot path)
-// ---------------------------------------------------------------------------
-// Same virtual-warp decomposition as k_pk_exact (4 warps per CTA, 8 CTAs per
-// band).  Built for the B200's issue rate:
+// 8 CTAs of 4 warps per band; the band's 32 virtual warps each take segments
+// vw, vw + 32, ... .  Built for the B200's issue rate:
 //   * every warp runs its own kP2Stages-deep ring of shared-memory stages;
 //     lane 0 fills each stage with two 1-D bulk copies (cp.async.bulk, the
 //     TMA engine): up to kP2ItemTiles consecutive tiles of a segment (4
@@ -682,9 +586,84 @@ __device__ __forceinline__ void p2_tile(uint32_t tw, uint32_t uw, uint32_t par, 
   }
 }
 
-template <int POL>
+// The transpose reduction of 16 per-lane AT values (m = 4 i + r) over the
+// warp, every stage in AT: afterwards lane l holds row m = l >> 1.
+template <typename AT>
+__device__ __forceinline__ AT seg_reduce16(const AT d[16], int lane) {
+  const bool b4 = lane & 16, b3 = lane & 8, b2 = lane & 4, b1 = lane & 2;
+  AT e[8];
+#pragma unroll
+  for (int j = 0; j < 8; ++j) {
+    const AT send = b4 ? d[j] : d[8 + j];
+    const AT mine = b4 ? d[8 + j] : d[j];
+    e[j] = mine + __shfl_xor_sync(0xFFFFFFFFu, send, 16);
+  }
+  AT f[4];
+#pragma unroll
+  for (int j = 0; j < 4; ++j) {
+    const AT send = b3 ? e[j] : e[4 + j];
+    const AT mine = b3 ? e[4 + j] : e[j];
+    f[j] = mine + __shfl_xor_sync(0xFFFFFFFFu, send, 8);
+  }
+  AT g[2];
+#pragma unroll
+  for (int j = 0; j < 2; ++j) {
+    const AT send = b2 ? f[j] : f[2 + j];
+    const AT mine = b2 ? f[2 + j] : f[j];
+    g[j] = mine + __shfl_xor_sync(0xFFFFFFFFu, send, 4);
+  }
+  const AT send = b1 ? g[0] : g[1];
+  const AT mine = b1 ? g[1] : g[0];
+  AT h = mine + __shfl_xor_sync(0xFFFFFFFFu, send, 2);
+  return h + __shfl_xor_sync(0xFFFFFFFFu, h, 1);
+}
+
+// Exact evaluation, one tile from shared memory: the four block-rows'
+// binary32 words, bit-exact with codec.decompress (int32 lift, exact
+// dequantisation, codec.py:128-218), times v in the policy's arithmetic,
+// added to se[4 i + r] in (row, column) order.
+// tw: stage address of the lane's first record word; vwa: of its v entry.
+template <int POL, typename AT>
+__device__ __forceinline__ void p2_tile_exact(uint32_t tw, uint32_t vwa, const pk::FieldPar* par, bool k2, bool kA,
+                                              bool kB, int We, uint32_t ebase, AT se[16]) {
+  float v[4];
+  {
+    uint4 t;
+    asm volatile("ld.shared.v4.u32 {%0, %1, %2, %3}, [%4];" : "=r"(t.x), "=r"(t.y), "=r"(t.z), "=r"(t.w) : "r"(vwa));
+    v[0] = __uint_as_float(t.x);
+    v[1] = __uint_as_float(t.y);
+    v[2] = __uint_as_float(t.z);
+    v[3] = __uint_as_float(t.w);
+  }
+#pragma unroll 1
+  for (int i = 0; i < 4; ++i) {
+    uint32_t a[pk::kFastWords];
+#pragma unroll
+    for (int kw = 0; kw < pk::kFastWords; ++kw)
+      asm volatile("ld.shared.u32 %0, [%1];" : "=r"(a[kw]) : "r"(tw + 512 * kw + 4 * i));
+    int32_t q[16];
+    pk_fields_int(a, par, k2, kA, kB, q);
+    float x[16];
+    pk::words_from_q(q, ebase + pk::field_edelta(a[0], We), x);
+#pragma unroll
+    for (int r = 0; r < 4; ++r) {
+      AT t = se[4 * i + r];
+#pragma unroll
+      for (int j = 0; j < 4; ++j) {
+        const float xv = x[4 * r + j];
+        if (POL == WHFF_POLICY_MIXED) t = __dadd_rn(t, (double)__fmul_rn(xv, v[j]));
+        else if (POL == WHFF_POLICY_SINGLE) t = __fadd_rn(t, __fmul_rn(xv, v[j]));
+        else t = __dadd_rn(t, __dmul_rn((double)xv, (double)v[j]));
+      }
+      se[4 * i + r] = t;
+    }
+  }
+}
+
+template <int EVAL, int POL>
 __global__ void __launch_bounds__(32 * kP2Warps, WHFF_P2_MINB) k_pk_gemv2(PkTable T, unsigned long long* status) {
   using AT = typename PkAcc<POL>::T;
+  constexpr bool kCoef = EVAL == WHFF_EVAL_COEFF;
   extern __shared__ __align__(128) uint8_t p2_smem[];
   const uint64_t gband = blockIdx.x / kP2Split;
   const int part = (int)(blockIdx.x % kP2Split);
@@ -833,7 +812,7 @@ __global__ void __launch_bounds__(32 * kP2Warps, WHFF_P2_MINB) k_pk_gemv2(PkTabl
 
   // parameters of the warp's segment k -> par[k & 1] (cp.async: no registers)
   auto prefetch_par = [&](int k) {
-    if (lane < 16 && k < (int)ctl_ld32(c_nseg)) {
+    if (kCoef && lane < 16 && k < (int)ctl_ld32(c_nseg)) {
       const pk::FieldPar* gp = reinterpret_cast<const pk::FieldPar*>(ctl_ld64(c_gpars));
       asm volatile("cp.async.cg.shared.global [%0], [%1], 16;" ::"r"(par0 + 256 * (k & 1) + 16 * lane),
                    "l"(gp + (uint64_t)kVW * 16 * k + lane) : "memory");
@@ -859,12 +838,21 @@ __global__ void __launch_bounds__(32 * kP2Warps, WHFF_P2_MINB) k_pk_gemv2(PkTabl
     __syncwarp();
     prefetch_par(k + 1);
     const uint32_t par = par0 + 256 * (k & 1);
-    // the segment's per-lane binary32 sums: s[h][r] = (block-row 2h, 2h + 1) x row r
+    // the segment's per-lane sums: coefficient, binary32 s[h][r] = (block-row
+    // 2h, 2h + 1) x row r; exact, AT se[4 i + r]
     float2 s[2][4];
+    AT se[16];
 #pragma unroll
     for (int h = 0; h < 2; ++h)
 #pragma unroll
       for (int r = 0; r < 4; ++r) s[h][r] = make_float2(0.0f, 0.0f);
+#pragma unroll
+    for (int m = 0; m < 16; ++m) se[m] = (AT)0;
+    if (!kCoef && !pk::seg_generic(S)) {
+      // exact evaluation: the integer-field parameters, computed here
+      if (lane < 16) W.par[k & 1][lane] = pk::field_param(S, lane);
+      __syncwarp();
+    }
     if (!pk::seg_generic(S)) {
       const bool k2 = pk::seg_k2(S), kA = pk::seg_kA(S), kB = pk::seg_kB(S);
       const bool gA = pk::seg_gA(S), gB = pk::seg_gB(S), m12 = pk::seg_m12(S);
@@ -875,6 +863,7 @@ __global__ void __launch_bounds__(32 * kP2Warps, WHFF_P2_MINB) k_pk_gemv2(PkTabl
       const uint32_t twb = (uint32_t)pk::tile_words(L) * 4;   // bytes per tile
       auto items = [&](auto SPECC) {
         constexpr int SPEC = decltype(SPECC)::value;
+        (void)SPEC;
         const int itl = p2_item_tiles(pk::rec_words(L));
         for (int tt = 0; tt < ntl; tt += itl) {
           const uint32_t bar = bar0 + 8 * cslot;
@@ -889,8 +878,12 @@ __global__ void __launch_bounds__(32 * kP2Warps, WHFF_P2_MINB) k_pk_gemv2(PkTabl
           const int nt = ntl - tt < itl ? ntl - tt : itl;
 #pragma unroll 1
           for (int it = 0; it < nt; ++it) {
+            if constexpr (kCoef)
               p2_tile<SPEC>(st + it * twb, st + kP2ItemTiles * kP2TileBytes + it * (pk::kTile * 16), par, m12,
                             k2, hasA, gA, kA, hasB, gB, kB, We, ebase_bits, s);
+            else
+              p2_tile_exact<POL, AT>(st + it * twb, st + kP2ItemTiles * kP2TileBytes + it * (pk::kTile * 16),
+                                     W.par[k & 1], k2, kA, kB, We, (uint32_t)pk::seg_emax_base(S), se);
           }
           // every lane has consumed the stage: refill it with the item kP2Stages ahead
           __syncwarp();
@@ -899,7 +892,8 @@ __global__ void __launch_bounds__(32 * kP2Warps, WHFF_P2_MINB) k_pk_gemv2(PkTabl
           cphase ^= cslot == 0 ? 1u : 0u;
         }
       };
-      if (m12 && !k2 && hasA && gA && !kA && hasB && gB && !kB) items(std::integral_constant<int, kSpecFull>());
+      if (!kCoef) items(std::integral_constant<int, kSpecAny>());
+      else if (m12 && !k2 && hasA && gA && !kA && hasB && gB && !kB) items(std::integral_constant<int, kSpecFull>());
       else if (m12 && !k2 && !hasA && !hasB) items(std::integral_constant<int, kSpecDC>());
       else items(std::integral_constant<int, kSpecAny>());
     } else {
@@ -919,6 +913,23 @@ __global__ void __launch_bounds__(32 * kP2Warps, WHFF_P2_MINB) k_pk_gemv2(PkTabl
           int32_t q[16];
           uint32_t ed;
           pk_generic_parse(&hdr(k), sbody + tt * TW, lane, i, q, &ed);
+          if constexpr (!kCoef) {
+            // (u holds v here: the exact evaluation's padded vector slice)
+            float x[16];
+            pk::words_from_q(q, (uint32_t)pk::seg_emax_base(S) + ed, x);
+#pragma unroll
+            for (int r = 0; r < 4; ++r) {
+              AT t = se[4 * i + r];
+#pragma unroll
+              for (int j = 0; j < 4; ++j) {
+                if (POL == WHFF_POLICY_MIXED) t = __dadd_rn(t, (double)__fmul_rn(x[4 * r + j], u[j]));
+                else if (POL == WHFF_POLICY_SINGLE) t = __fadd_rn(t, __fmul_rn(x[4 * r + j], u[j]));
+                else t = __dadd_rn(t, __dmul_rn((double)x[4 * r + j], (double)u[j]));
+              }
+              se[4 * i + r] = t;
+            }
+            continue;
+          }
           float w[4];
           w[0] = __fmul_rn(__int2float_rn(q[0]), u[0]);
           w[1] = w[2] = w[3] = 0.0f;
@@ -937,26 +948,28 @@ __global__ void __launch_bounds__(32 * kP2Warps, WHFF_P2_MINB) k_pk_gemv2(PkTabl
       }
     }
     // the segment's sums over the warp (row m of the band: m = 4 i + r)
-    acc = acc + seg_reduce<AT>(s, lane);
+    if constexpr (kCoef) acc = acc + seg_reduce<AT>(s, lane);
+    else acc = acc + seg_reduce16<AT>(se, lane);
     if (S.exc_count) pk_exceptions<POL, AT>(J.p, J.v, band, S.exc_begin, S.exc_count, lane, W.rs);
   }
   asm volatile("cp.async.wait_group 0;" ::: "memory");
-  pk_band_epilogue<WHFF_EVAL_COEFF, POL, AT>(T, J, J.p, gband, band, pk::band_rows(J.p.g, band), vw, lane, &acc, true,
-                                             W.rs, status);
+  pk_band_epilogue<EVAL, POL, AT>(T, J, J.p, gband, band, pk::band_rows(J.p.g, band), vw, lane, &acc, true, W.rs,
+                                  status);
 }
 
-template <int POL>
+template <int EVAL, int POL>
 static cudaError_t p2_launch(const PkTable& T, unsigned long long* status, cudaStream_t cs) {
   using AT = typename PkAcc<POL>::T;
   const size_t smem = sizeof(P2Warp<AT>) * kP2Warps;
   static bool attr = false;   // set once per process (the attribute is per function)
   if (!attr) {
-    cudaError_t e = cudaFuncSetAttribute(k_pk_gemv2<POL>, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem);
+    cudaError_t e =
+        cudaFuncSetAttribute(k_pk_gemv2<EVAL, POL>, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem);
     if (e != cudaSuccess) return e;
     attr = true;
   }
   const unsigned blocks = (unsigned)(T.total_bands * kP2Split);
-  k_pk_gemv2<POL><<<blocks, 32 * kP2Warps, smem, cs>>>(T, status);
+  k_pk_gemv2<EVAL, POL><<<blocks, 32 * kP2Warps, smem, cs>>>(T, status);
   return cudaGetLastError();
 }
 
@@ -1052,21 +1065,14 @@ cudaError_t pk_launch_words(const PkView& v, uint64_t nexc, float* out, uint64_t
   return cudaGetLastError();
 }
 
-static void pk_exact_pol(int policy, const PkTable& T, unsigned long long* status, cudaStream_t cs) {
-  const unsigned blocks = (unsigned)(T.total_bands * kPkSplit);
-  const unsigned threads = 32 * kPkWarps;
-  if (policy == WHFF_POLICY_SINGLE) k_pk_exact<WHFF_POLICY_SINGLE><<<blocks, threads, 0, cs>>>(T, status);
-  else if (policy == WHFF_POLICY_MIXED) k_pk_exact<WHFF_POLICY_MIXED><<<blocks, threads, 0, cs>>>(T, status);
-  else k_pk_exact<WHFF_POLICY_DOUBLE><<<blocks, threads, 0, cs>>>(T, status);
-}
-
 cudaError_t pk_launch_gemv(int eval, int policy, const PkTable& T, unsigned long long* status,
                            cudaStream_t cs) {
   if (T.total_bands == 0) return cudaSuccess;
   if (eval == WHFF_EVAL_COEFF) {
-    if (policy == WHFF_POLICY_SINGLE) return p2_launch<WHFF_POLICY_SINGLE>(T, status, cs);
-    return p2_launch<WHFF_POLICY_MIXED>(T, status, cs);
+    if (policy == WHFF_POLICY_SINGLE) return p2_launch<WHFF_EVAL_COEFF, WHFF_POLICY_SINGLE>(T, status, cs);
+    return p2_launch<WHFF_EVAL_COEFF, WHFF_POLICY_MIXED>(T, status, cs);
   }
-  pk_exact_pol(policy, T, status, cs);
-  return cudaGetLastError();
+  if (policy == WHFF_POLICY_SINGLE) return p2_launch<WHFF_EVAL_EXACT, WHFF_POLICY_SINGLE>(T, status, cs);
+  if (policy == WHFF_POLICY_MIXED) return p2_launch<WHFF_EVAL_EXACT, WHFF_POLICY_MIXED>(T, status, cs);
+  return p2_launch<WHFF_EVAL_EXACT, WHFF_POLICY_DOUBLE>(T, status, cs);
 }

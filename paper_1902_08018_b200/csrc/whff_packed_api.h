@@ -49,9 +49,7 @@ struct PkTable {
 };
 
 
-constexpr int kPkWarps = 8;                 // warps per CTA of k_pk_gemv
 constexpr int kPkVW = 32;                   // virtual warps per band
-constexpr int kPkSplit = kPkVW / kPkWarps;  // CTAs per band
 
 // host launchers (whff_packed.cu); all asynchronous on `cs`
 cudaError_t pk_launch_stats(const struct StreamView& s, const whff::pk::Geom& g, whff::pk::Seg* segs,

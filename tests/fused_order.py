@@ -299,38 +299,36 @@ def packed_model(orc, stream, v, policy="mixed", evaluation="coefficient"):
         T = T.astype(acc_t)
     out = np.zeros(nband * 16, np.float32)
     for band in range(nband):
-        D = np.zeros((32, 32, 4, 4), acc_t)           # [vw, lane, i, r]
         R = np.zeros((32, 16), acc_t)                 # [vw, 4 i + r]
-        staged = evaluation == "coefficient"     # k_pk_gemv2's order
-        if staged:
-            # per segment: per-lane binary32 sums over the segment's tiles (one
-            # FMA-rounding per term), then the warp's transpose reduction over
-            # the 32 lanes (the xor-16..1 butterfly) in binary64 (single:
-            # binary32), accumulated per segment in the virtual warp's order
-            Dv_acc = np.zeros((32, 16), acc_t)
+        # k_pk_gemv2's order, both evaluations: per segment, per-lane sums over
+        # the segment's tiles -- coefficient: binary32 (one FMA rounding per
+        # term), reduced over the warp with a binary32 xor-16 stage and then
+        # xor 8, 4, 2, 1 in binary64; exact: the policy's accumulator (binary64
+        # for mixed), reduced over the warp in it -- accumulated per segment
+        # in the virtual warp's order
+        Dv_acc = np.zeros((32, 16), acc_t)
         for vw in range(32):
             for sb in range(vw, nsegb, 32):
-                if staged:
-                    Sg = np.zeros((32, 4, 4), np.float32)          # [lane, i, r]
+                Sg = np.zeros((32, 4, 4), np.float32)          # [lane, i, r] (coefficient)
+                Se = np.zeros((32, 4, 4), acc_t)               # [lane, i, r] (exact)
                 for tt in range(8):
                     cs = (8 * sb + tt) * 32 + np.arange(32)
                     for i in range(4):
                         b = 4 * band + i
-                        if staged:
+                        if evaluation == "coefficient":
                             Sg[:, i, :] = (Sg[:, i, :] + T[b, cs, :].astype(np.float32)).astype(np.float32)
-                        elif evaluation == "coefficient":
-                            raise AssertionError("unreachable")
                         else:
                             m = ~exc[b, cs]
                             for r in range(4):
                                 for j in range(4):
-                                    D[vw, :, i, r] = np.where(m, D[vw, :, i, r] + Pa[b, cs, r, j],
-                                                              D[vw, :, i, r])
-                if staged:
+                                    Se[:, i, r] = np.where(m, Se[:, i, r] + Pa[b, cs, r, j], Se[:, i, r])
+                if evaluation == "coefficient":
                     # seg_reduce: xor-16 stage in binary32, then xor 8, 4, 2, 1
                     Dseg = Sg.reshape(32, 16)                          # [lane, m = 4 i + r]
                     X1 = (Dseg + Dseg[np.arange(32) ^ 16]).astype(np.float32).astype(acc_t)
                     Dv_acc[vw] = Dv_acc[vw] + _butterfly(np.moveaxis(X1, 0, -1), (8, 4, 2, 1))
+                else:
+                    Dv_acc[vw] = Dv_acc[vw] + _butterfly(np.moveaxis(Se.reshape(32, 16), 0, -1))
                 for tt in range(8):
                     for i in range(4):
                         b = 4 * band + i
@@ -341,10 +339,7 @@ def packed_model(orc, stream, v, policy="mixed", evaluation="coefficient"):
                             for r in range(4):
                                 p = Pa[b, col, r]
                                 R[vw, 4 * i + r] = R[vw, 4 * i + r] + ((p[0] + p[1]) + (p[2] + p[3]))
-        if staged:
-            Dv = Dv_acc.reshape(32, 4, 4)
-        else:
-            Dv = _butterfly(np.moveaxis(D, 1, -1))     # [vw, i, r]
+        Dv = Dv_acc.reshape(32, 4, 4)
         Dt = _butterfly(np.moveaxis(Dv, 0, -1))        # [i, r]
         Rt = _butterfly(np.moveaxis(R, 0, -1))         # [16]
         for i in range(4):
