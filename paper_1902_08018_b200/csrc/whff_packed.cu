@@ -782,7 +782,9 @@ __global__ void __launch_bounds__(32 * kP2Warps, WHFF_P2_MINB) k_pk_gemv2(PkTabl
     const int it = p2_item_tiles((int)(ptw >> 7));
     const int nt = pntl - pt < it ? pntl - pt : it;
     // the whole (converged) warp runs this with warp-uniform operands; one
-    // elected lane arms the barrier and issues the copies (no per-lane loop)
+    // elected lane arms the barrier and issues the copies (no per-lane loop).
+    // The records are read once (L2 evict-first); the U slices are shared by
+    // every band of the launch (default policy: they stay in L2)
     const uint4 A = ctl_ld128(c_A);
     const uint64_t pbody = u64_of(A.x, A.y), usrc = u64_of(A.z, A.w), policy = ctl_ld64(c_policy);
     const uint32_t pslot = B.w;
@@ -794,7 +796,7 @@ __global__ void __launch_bounds__(32 * kP2Warps, WHFF_P2_MINB) k_pk_gemv2(PkTabl
         "elect.sync _|p, 0xffffffff;\n"
         "@p mbarrier.arrive.expect_tx.shared::cta.b64 _, [%1], %6;\n"
         "@p cp.async.bulk.shared::cluster.global.mbarrier::complete_tx::bytes.L2::cache_hint [%0], [%2], %4, [%1], %7;\n"
-        "@p cp.async.bulk.shared::cluster.global.mbarrier::complete_tx::bytes.L2::cache_hint [%8], [%3], %5, [%1], %7;\n"
+        "@p cp.async.bulk.shared::cluster.global.mbarrier::complete_tx::bytes [%8], [%3], %5, [%1];\n"
         "}\n" ::"r"(st), "r"(bar), "l"(pbody), "l"(usrc), "r"(tb), "r"(ub), "r"(tb + ub), "l"(policy),
         "r"(st + kP2ItemTiles * kP2TileBytes)
         : "memory");
