@@ -795,6 +795,138 @@ __global__ void k_gemv_seq(const float* A, uint64_t lda, uint64_t rows, uint64_t
   }
 }
 
+// The same strict left-to-right order, one lane per row, fed by bulk copies.
+// Each row is a serial chain of adds: on B200 a dependent binary64 add is 8
+// cycles, and a conversion or product feeding it makes 13 (mixed) to 18
+// (double) cycles per element from registers (5 for single), so the
+// kernel's floor is cols x that, and everything else must stay off the
+// chain.  Each warp owns `nr` <= 32 rows and its own ring of kSqStages
+// shared-memory stages; a stage holds a sq_cols(nr)-column slice of each of
+// the warp's rows (one cp.async.bulk per lane, rows padded to an odd number
+// of 16-byte chunks so the lanes' 16-byte reads do not conflict) and the
+// matching slice of v, all completing on the stage's mbarrier.  Four warps
+// per CTA, one per SM sub-partition, and `nr` chosen so the warps cover the
+// 148 x 4 sub-partitions once: two chains on one sub-partition would share
+// its FP64 pipe and run at half speed.  Needs A, v 16-byte aligned and
+// lda % 4 == 0; the last cols % 4 columns are read from global memory.
+constexpr int kSqStages = 4;
+constexpr int kSqWarps = 4;
+// columns per stage (a multiple of 8: odd 16-byte row stride)
+__host__ __device__ constexpr int sq_cols(int nr) {
+  return nr <= 1 ? 1024 : nr <= 2 ? 512 : nr <= 4 ? 256 : nr <= 8 ? 128 : 64;
+}
+__host__ __device__ constexpr int sq_row_bytes(int nr) { return sq_cols(nr) * 4 + 16; }
+__host__ __device__ constexpr int sq_stage_bytes(int nr) { return nr * sq_row_bytes(nr) + sq_cols(nr) * 4; }
+__host__ __device__ constexpr int sq_warp_bytes(int nr) {
+  return (kSqStages * sq_stage_bytes(nr) + kSqStages * 8 + 127) / 128 * 128;
+}
+
+template <int POL>
+__global__ void __launch_bounds__(32 * kSqWarps) k_gemv_seq_staged(const float* A, uint64_t lda, uint64_t rows,
+                                                                   uint64_t cols, const float* v, float* y, int nr) {
+  extern __shared__ __align__(128) uint8_t sq_smem[];
+  const int lane = threadIdx.x & 31, warp = threadIdx.x >> 5;
+  const uint64_t r0 = ((uint64_t)blockIdx.x * kSqWarps + warp) * nr;
+  if (r0 >= rows) return;
+  const int nrow = rows - r0 < (uint64_t)nr ? (int)(rows - r0) : nr;
+  const int rl = lane < nrow ? lane : 0;   // idle lanes shadow the first row
+  const int sb = sq_stage_bytes(nr), kc = sq_cols(nr), rb = sq_row_bytes(nr);
+  const uint32_t st0 = (uint32_t)__cvta_generic_to_shared(sq_smem) + warp * sq_warp_bytes(nr);
+  const uint32_t bar0 = st0 + kSqStages * sb;
+  const uint32_t voff = nr * rb;
+  const uint64_t cmain = cols & ~3ull;
+  const uint64_t nchunk = (cmain + kc - 1) / kc;
+  if (lane == 0)
+    for (int s = 0; s < kSqStages; ++s)
+      asm volatile("mbarrier.init.shared::cta.b64 [%0], 1;" ::"r"(bar0 + 8 * s) : "memory");
+  asm volatile("fence.mbarrier_init.release.cluster;" ::: "memory");
+  __syncwarp();
+  auto issue = [&](uint64_t c) {
+    if (c >= nchunk) return;
+    const int s = (int)(c % kSqStages);
+    const uint64_t j0 = c * kc;
+    const uint32_t bytes = (uint32_t)((cmain - j0 < (uint64_t)kc ? cmain - j0 : (uint64_t)kc) * 4);
+    const uint32_t st = st0 + s * sb, bar = bar0 + 8 * s;
+    if (lane == 0)
+      asm volatile("mbarrier.arrive.expect_tx.shared::cta.b64 _, [%0], %1;" ::"r"(bar), "r"(bytes * (nrow + 1))
+                   : "memory");
+    __syncwarp();
+    if (lane < nrow)
+      asm volatile("cp.async.bulk.shared::cluster.global.mbarrier::complete_tx::bytes [%0], [%1], %2, [%3];"
+                   ::"r"(st + lane * rb), "l"(A + (r0 + lane) * lda + j0), "r"(bytes), "r"(bar)
+                   : "memory");
+    if (lane == 0)
+      asm volatile("cp.async.bulk.shared::cluster.global.mbarrier::complete_tx::bytes [%0], [%1], %2, [%3];"
+                   ::"r"(st + voff), "l"(v + j0), "r"(bytes), "r"(bar)
+                   : "memory");
+  };
+  for (int s = 0; s < kSqStages; ++s) issue(s);
+  using AT = typename std::conditional<POL == WHFF_POLICY_SINGLE, float, double>::type;
+  AT acc = 0;
+  auto add = [&](float a, float b) {
+    if (POL == WHFF_POLICY_SINGLE) acc = __fadd_rn(acc, __fmul_rn(a, b));
+    else if (POL == WHFF_POLICY_MIXED) acc = __dadd_rn(acc, (double)__fmul_rn(a, b));
+    else acc = __dadd_rn(acc, __dmul_rn((double)a, (double)b));
+  };
+  auto lds4 = [&](uint32_t addr) {
+    float4 r;
+    asm volatile("ld.shared.v4.f32 {%0, %1, %2, %3}, [%4];" : "=f"(r.x), "=f"(r.y), "=f"(r.z), "=f"(r.w)
+                 : "r"(addr));
+    return r;
+  };
+  auto add4 = [&](const float4& a, const float4& b) {
+    add(a.x, b.x);
+    add(a.y, b.y);
+    add(a.z, b.z);
+    add(a.w, b.w);
+  };
+  for (uint64_t c = 0; c < nchunk; ++c) {
+    const int s = (int)(c % kSqStages);
+    const uint32_t phase = (uint32_t)((c / kSqStages) & 1);
+    const uint32_t bar = bar0 + 8 * s;
+    asm volatile(
+        "{\n"
+        ".reg .pred p;\n"
+        "SQ_WAIT_%=:\n"
+        "mbarrier.try_wait.parity.shared::cta.b64 p, [%0], %1;\n"
+        "@!p bra SQ_WAIT_%=;\n"
+        "}\n" ::"r"(bar), "r"(phase) : "memory");
+    const uint32_t ra = st0 + s * sb + rl * rb, va = st0 + s * sb + voff;
+    const int n4 = (int)((cmain - c * kc < (uint64_t)kc ? cmain - c * kc : (uint64_t)kc) / 4);
+    // 32 columns per step: the 16 shared loads issue together, then the
+    // chain runs through them (one exposed load latency per 32 columns)
+    int k = 0;
+    for (; k + 8 <= n4; k += 8) {
+      float4 a[8], b[8];
+#pragma unroll
+      for (int u = 0; u < 8; ++u) {
+        a[u] = lds4(ra + 16 * (k + u));
+        b[u] = lds4(va + 16 * (k + u));
+      }
+#pragma unroll
+      for (int u = 0; u < 8; ++u) add4(a[u], b[u]);
+    }
+    for (; k < n4; ++k) add4(lds4(ra + 16 * k), lds4(va + 16 * k));
+    __syncwarp();   // every lane is done with the stage before it is refilled
+    issue(c + kSqStages);
+  }
+  if (lane < nrow) {
+    const float* row = A + (r0 + lane) * lda;
+    for (uint64_t j = cmain; j < cols; ++j) add(row[j], v[j]);
+    y[r0 + lane] = (float)acc;
+  }
+}
+
+// rows per warp: one chain set per SM sub-partition (148 x 4), at most 32
+static int seq_rows_per_warp(uint64_t rows) {
+  const uint64_t want = (rows + 148 * kSqWarps - 1) / (148 * kSqWarps);
+  return want >= 32 ? 32 : (int)std::max<uint64_t>(want, 1);
+}
+
+static bool seq_staged_ok(const float* A, uint64_t lda, const float* v) {
+  return ((uintptr_t)A % 16 == 0) && ((uintptr_t)v % 16 == 0) && lda % 4 == 0;
+}
+
 // mpgemv.gemv_oracle (mpgemv.py:64-69) on binary64 inputs: binary64
 // products, sequential binary64 sum (np.cumsum order); one thread per row.
 __global__ void k_gemv_oracle64(const double* A, uint64_t lda, uint64_t rows, uint64_t cols, const double* v,
@@ -2370,7 +2502,16 @@ static whff_status_t gemv_pol(const float* A, uint64_t lda, uint64_t rows, uint6
                               const float* v, float* y, int shape, int fanout, void* ws, size_t wsb,
                               cudaStream_t cs) {
   if (shape == WHFF_SHAPE_SEQUENTIAL) {
-    k_gemv_seq<POL, false><<<grid_for(rows, 64), 64, 0, cs>>>(A, lda, rows, cols, v, y, nullptr);
+    if (seq_staged_ok(A, lda, v)) {
+      static std::atomic<uint64_t> attr{0};
+      WCK(ensure_dyn_smem(k_gemv_seq_staged<POL>, kSqWarps * sq_warp_bytes(32), attr));
+      const int nr = seq_rows_per_warp(rows);
+      const uint64_t nw = (rows + nr - 1) / nr;
+      k_gemv_seq_staged<POL><<<(unsigned)((nw + kSqWarps - 1) / kSqWarps), 32 * kSqWarps, kSqWarps * sq_warp_bytes(nr),
+                               cs>>>(A, lda, rows, cols, v, y, nr);
+    } else {
+      k_gemv_seq<POL, false><<<grid_for(rows, 64), 64, 0, cs>>>(A, lda, rows, cols, v, y, nullptr);
+    }
     WCK_LAUNCH("gemv sequential");
     return WHFF_OK;
   }

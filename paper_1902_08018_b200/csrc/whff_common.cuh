@@ -6,11 +6,29 @@
 
 #include <cuda_runtime.h>
 
+#include <atomic>
+#include <cstdint>
+
 #include "../../include/whff_b200.h"
 #include "whff_decode.cuh"
 #include "whff_relayout.cuh"
 
 using namespace whff;
+
+// Opt a kernel into more than 48 KB of dynamic shared memory, once per
+// device (the attribute belongs to the function's instance in the current
+// device's context).  `done` is the kernel's own per-device bitmask.
+template <typename Kernel>
+static cudaError_t ensure_dyn_smem(Kernel* k, int bytes, std::atomic<uint64_t>& done) {
+  int dev = 0;
+  cudaError_t e = cudaGetDevice(&dev);
+  if (e != cudaSuccess) return e;
+  const uint64_t bit = 1ull << (dev & 63);
+  if (done.load(std::memory_order_acquire) & bit) return cudaSuccess;
+  e = cudaFuncSetAttribute(k, cudaFuncAttributeMaxDynamicSharedMemorySize, bytes);
+  if (e == cudaSuccess) done.fetch_or(bit, std::memory_order_acq_rel);
+  return e;
+}
 
 // ---------------------------------------------------------------------------
 // device view of a stream

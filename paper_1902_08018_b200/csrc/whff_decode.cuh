@@ -668,29 +668,25 @@ WHFF_HD float dequant_slow(int32_t q, int k) {
 }
 
 
-// Decoded block -> 16 binary32 words in raster order (codec.py:209-218).
-WHFF_HD void reconstruct_words(const Decoded& d, float out[16]) {
-  if (d.raw) {                               // codec.py:215-217
+// Signed sequency-order coefficients (|q| < 2^27) -> the 16 lifted integers
+// in raster order (codec.py:145-150).
+WHFF_HD void lift_signed(const int32_t q[16], int32_t t[16]) {
 #pragma unroll
-    for (int i = 0; i < 16; ++i) out[i] = as_float(d.mag[i]);
-    return;
-  }
-  int32_t t[16];
-#pragma unroll
-  for (int c = 0; c < 16; ++c) {
-    const int32_t v = (int32_t)d.mag[c];
-    t[seq_pos(c)] = ((d.negm >> c) & 1u) ? -v : v;   // codec.py:210-212
-  }
+  for (int c = 0; c < 16; ++c) t[seq_pos(c)] = q[c];
 #pragma unroll
   for (int i = 0; i < 4; ++i) inv_lift(t[i], t[4 + i], t[8 + i], t[12 + i]);          // columns
 #pragma unroll
   for (int i = 0; i < 4; ++i) inv_lift(t[4 * i], t[4 * i + 1], t[4 * i + 2], t[4 * i + 3]);  // rows
-  if (d.emax == 0) {                         // codec.py:205
+}
+
+// Lifted integers + emax code -> binary32 words (codec.py:201-206).
+WHFF_HD void dequant_words(const int32_t t[16], uint32_t emax, float out[16]) {
+  if (emax == 0) {                         // codec.py:205
 #pragma unroll
     for (int i = 0; i < 16; ++i) out[i] = 0.0f;
     return;
   }
-  const int k = (int)d.emax - kEmaxBias - kQuantBits;
+  const int k = (int)emax - kEmaxBias - kQuantBits;
   if (dequant_fast_ok(k)) {
     const float s = scale_f32(k);
 #pragma unroll
@@ -699,6 +695,30 @@ WHFF_HD void reconstruct_words(const Decoded& d, float out[16]) {
 #pragma unroll
     for (int i = 0; i < 16; ++i) out[i] = dequant_slow(t[i], k);
   }
+}
+
+// Signed coefficients + emax code -> the 16 binary32 words: the part of
+// reconstruct_words after the sign, shared with the packed layout.
+WHFF_HD void words_from_signed(const int32_t q[16], uint32_t emax, float out[16]) {
+  int32_t t[16];
+  lift_signed(q, t);
+  dequant_words(t, emax, out);
+}
+
+// Decoded block -> 16 binary32 words in raster order (codec.py:209-218).
+WHFF_HD void reconstruct_words(const Decoded& d, float out[16]) {
+  if (d.raw) {                               // codec.py:215-217
+#pragma unroll
+    for (int i = 0; i < 16; ++i) out[i] = as_float(d.mag[i]);
+    return;
+  }
+  int32_t q[16];
+#pragma unroll
+  for (int c = 0; c < 16; ++c) {
+    const int32_t v = (int32_t)d.mag[c];
+    q[c] = ((d.negm >> c) & 1u) ? -v : v;   // codec.py:210-212
+  }
+  words_from_signed(q, d.emax, out);
 }
 
 }  // namespace whff

@@ -641,21 +641,47 @@ __device__ __forceinline__ void p2_tile_exact(uint32_t tw, uint32_t vwa, const p
 #pragma unroll
     for (int kw = 0; kw < pk::kFastWords; ++kw)
       asm volatile("ld.shared.u32 %0, [%1];" : "=r"(a[kw]) : "r"(tw + 512 * kw + 4 * i));
-    int32_t q[16];
+    int32_t q[16], t[16];
     pk_fields_int(a, par, k2, kA, kB, q);
+    lift_signed(q, t);
+    // dequantisation (codec.py:201-206) on the packed pipe when the scale
+    // is a normal-or-subnormal binary32 power of two (single rounding,
+    // as dequant_words); otherwise the binary64 path
+    const uint32_t emax = ebase + pk::field_edelta(a[0], We);
+    const int k = (int)emax - kEmaxBias - kQuantBits;
     float x[16];
-    pk::words_from_q(q, ebase + pk::field_edelta(a[0], We), x);
+    if (emax != 0u && dequant_fast_ok(k)) {
+      const float s = scale_f32(k);
+#pragma unroll
+      for (int m = 0; m < 16; m += 2) {
+        const float2 w = __fmul2_rn(make_float2((float)t[m], (float)t[m + 1]), make_float2(s, s));
+        x[m] = w.x;
+        x[m + 1] = w.y;
+      }
+    } else {
+      dequant_words(t, emax, x);
+    }
 #pragma unroll
     for (int r = 0; r < 4; ++r) {
-      AT t = se[4 * i + r];
+      AT acc = se[4 * i + r];
+      if (POL == WHFF_POLICY_DOUBLE) {
 #pragma unroll
-      for (int j = 0; j < 4; ++j) {
-        const float xv = x[4 * r + j];
-        if (POL == WHFF_POLICY_MIXED) t = __dadd_rn(t, (double)__fmul_rn(xv, v[j]));
-        else if (POL == WHFF_POLICY_SINGLE) t = __fadd_rn(t, __fmul_rn(xv, v[j]));
-        else t = __dadd_rn(t, __dmul_rn((double)xv, (double)v[j]));
+        for (int j = 0; j < 4; ++j) acc = __dadd_rn(acc, __dmul_rn((double)x[4 * r + j], (double)v[j]));
+      } else {
+        // binary32 products two at a time, added in column order
+#pragma unroll
+        for (int j = 0; j < 4; j += 2) {
+          const float2 p = __fmul2_rn(make_float2(x[4 * r + j], x[4 * r + j + 1]), make_float2(v[j], v[j + 1]));
+          if (POL == WHFF_POLICY_MIXED) {
+            acc = __dadd_rn(acc, (double)p.x);
+            acc = __dadd_rn(acc, (double)p.y);
+          } else {
+            acc = __fadd_rn(acc, p.x);
+            acc = __fadd_rn(acc, p.y);
+          }
+        }
       }
-      se[4 * i + r] = t;
+      se[4 * i + r] = acc;
     }
   }
 }
@@ -963,13 +989,9 @@ template <int EVAL, int POL>
 static cudaError_t p2_launch(const PkTable& T, unsigned long long* status, cudaStream_t cs) {
   using AT = typename PkAcc<POL>::T;
   const size_t smem = sizeof(P2Warp<AT>) * kP2Warps;
-  static bool attr = false;   // set once per process (the attribute is per function)
-  if (!attr) {
-    cudaError_t e =
-        cudaFuncSetAttribute(k_pk_gemv2<EVAL, POL>, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem);
-    if (e != cudaSuccess) return e;
-    attr = true;
-  }
+  static std::atomic<uint64_t> attr{0};
+  const cudaError_t e = ensure_dyn_smem(k_pk_gemv2<EVAL, POL>, (int)smem, attr);
+  if (e != cudaSuccess) return e;
   const unsigned blocks = (unsigned)(T.total_bands * kP2Split);
   k_pk_gemv2<EVAL, POL><<<blocks, 32 * kP2Warps, smem, cs>>>(T, status);
   return cudaGetLastError();

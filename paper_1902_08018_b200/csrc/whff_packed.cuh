@@ -267,15 +267,7 @@ WHFF_HD void signed_coefs(const Decoded& d, int32_t q[16]) {
 
 // Words of a block from its signed coefficients (as reconstruct_words).
 WHFF_HD void words_from_q(const int32_t q[16], uint32_t emax, float out[16]) {
-  Decoded d;
-  d.raw = 0;
-  d.emax = emax;
-  d.negm = 0;
-  for (int c = 0; c < 16; ++c) {
-    d.mag[c] = (uint32_t)(q[c] < 0 ? -q[c] : q[c]);
-    if (q[c] < 0) d.negm |= 1u << c;
-  }
-  reconstruct_words(d, out);
+  words_from_signed(q, emax, out);
 }
 
 // ---------------------------------------------------------------------------

@@ -106,3 +106,34 @@ def test_gemv_oracle_keeps_binary64_inputs(rng):
     want = np.cumsum(m * v, axis=1, dtype=np.float64)[:, -1]
     got = gemv_oracle(m, v)
     assert got.dtype == np.float64 and np.array_equal(got, want)
+
+
+@pytest.mark.parametrize("rows,cols,pad", [
+    (70, 1000, 0),       # staged: seven full 128-column stages + a 104-column one
+    (33, 128, 0),        # one stage, a row block with a single row
+    (5, 3, 0),           # no staged columns: global-memory tail only
+    (37, 1003, 0),       # lda % 4 != 0: the per-thread kernel
+    (40, 1003, 1),       # strided rows (lda 1004): staged + 3-column tail
+    (600, 515, 1),       # 2 rows per warp, strided
+    (5000, 260, 0),      # 9 rows per warp, a partial last warp
+    (19000, 100, 0),     # 32 rows per warp
+    (378, 256000, 0),    # one paper slit
+])
+def test_sequential_kernels_bit_exact_vs_oracle(orc, rows, cols, pad):
+    """K:24-47 strict left-to-right order, on every sequential kernel path
+    (the bulk-copy staged kernel at 1..32 rows per warp, and the per-thread
+    fallback for unaligned rows)."""
+    import torch
+    from paper_1902_08018_b200.mpgemv import gemv_device
+    g = np.random.default_rng(rows * 7919 + cols)
+    base = (g.standard_normal((rows, cols + pad)) * np.exp(g.uniform(-20, 20, (rows, 1)))).astype(np.float32)
+    m = np.ascontiguousarray(base[:, :cols])
+    v = g.standard_normal(cols).astype(np.float32)
+    mt = torch.from_numpy(base).cuda()[:, :cols]
+    vt = torch.from_numpy(v).cuda()
+    for pol in ("mixed", "single", "double"):
+        if cols > 100000 and pol != "mixed":
+            continue
+        got = gemv_device(mt, vt, pol, "sequential").cpu().numpy()
+        want = orc.gemv_kernel(m, v, pol, "sequential")
+        assert np.array_equal(got.view(np.uint32), want.view(np.uint32)), (rows, cols, pad, pol)
