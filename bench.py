@@ -57,6 +57,10 @@ def parse():
     ap.add_argument("--rows", type=int, default=378)
     ap.add_argument("--S", type=int, default=256000)
     ap.add_argument("--grid", type=int, default=608)
+    ap.add_argument("--preset", choices=["paper", "mesh4x"], default=None,
+                    help="paper: configs[2]/[3] (S = 256,000, T = 608^2, the defaults); "
+                         "mesh4x: the configs[4] sustained workload (S = 1,024,000, "
+                         "T = 1216^2, 1000 latency steps), unchanged at --gpus 8")
     ap.add_argument("--distinct", type=int, default=0,
                     help="distinct slit contents per axis (0 = all); the rest are "
                          "physically distinct HBM copies")
@@ -76,7 +80,12 @@ def parse():
     ap.add_argument("--latency-steps", type=int, default=1000,
                     help="extra back-to-back steps (after the timed region) whose per-step "
                          "CUDA-event times give latency p50/p99/max (SURVEY 8d: >= 1000)")
-    return ap.parse_args()
+    args = ap.parse_args()
+    if args.preset == "mesh4x":
+        args.S, args.grid, args.latency_steps = 1024000, 1216, max(args.latency_steps, 1000)
+    elif args.preset == "paper":
+        args.S, args.grid = 256000, 608
+    return args
 
 
 def parse_mode(s):

@@ -1,7 +1,9 @@
 """Small runs of every packed-layout kernel for compute-sanitizer
 (memcheck / racecheck / synccheck / initcheck): the staged coefficient
 kernel (mixed, single; single calls, row ranges, a plan), the exact
-evaluation, decode-only, the packer -- on smooth and random streams.
+evaluation, decode-only, the packer -- on smooth and random streams -- and
+the bulk-copy staged sequential GEMV (1, 2, 9 and 32 rows per warp, a
+strided matrix with a column tail).
 Usage: compute-sanitizer --tool <tool> python tools/san_probe.py"""
 import os
 import sys
@@ -40,5 +42,12 @@ plan = GemvPlan([(streams[0], v, out[:streams[0].rows], 0, streams[0].rows),
                  (streams[0].clone(), v, out[streams[0].rows:], 0, streams[0].rows)], "mixed", "coefficient")
 st = _lib.status_word()
 plan.launch(st)
+torch.cuda.synchronize()
+from paper_1902_08018_b200.mpgemv import gemv_device  # noqa: E402
+for rows, cols, pad in ((70, 1000, 0), (600, 515, 1), (5000, 260, 0), (19000, 68, 0)):
+    base = torch.from_numpy(rng.standard_normal((rows, cols + pad)).astype(np.float32)).cuda()
+    vv = torch.from_numpy(rng.standard_normal(cols).astype(np.float32)).cuda()
+    for pol in ("mixed", "single", "double"):
+        gemv_device(base[:, :cols], vv, pol, "sequential")
 torch.cuda.synchronize()
 print("san_probe ok")
