@@ -246,10 +246,10 @@ __device__ __forceinline__ void pk_band_epilogue(const PkTable& T, const PkJob& 
 // 8 CTAs of 4 warps per band; the band's 32 virtual warps each take segments
 // vw, vw + 32, ... .  Built for the B200's issue rate:
 //   * every warp runs its own kP2Stages-deep ring of shared-memory stages;
-//     lane 0 fills each stage with two 1-D bulk copies (cp.async.bulk, the
-//     TMA engine): up to kP2ItemTiles consecutive tiles of a segment (4
-//     block-rows x 32 block-columns of records each, word-major, contiguous
-//     in HBM) and their slice of U = G^T v, completing on the stage's
+//     one elected lane fills each stage with two 1-D bulk copies
+//     (cp.async.bulk, the TMA engine): up to p2_item_tiles(R) consecutive
+//     tiles of a segment (4 block-rows x 32 block-columns of records each,
+//     word-major, contiguous in HBM) and their slice of U = G^T v, completing on the stage's
 //     mbarrier: no registers hold loads in flight and the copies of the next
 //     items overlap the decode of this one;
 //   * one 16-byte shared load per record word gives that word of all four
@@ -263,9 +263,9 @@ __device__ __forceinline__ void pk_band_epilogue(const PkTable& T, const PkJob& 
 //     the two large AC coefficients only) besides the general one;
 //   * per segment (8 tiles) each lane sums its 2^k (Q u) terms per (block-
 //     row, row) in binary32; at the segment's end the warp reduces the 16
-//     sums over its 32 lanes in binary64 with a transpose reduction (8 + 4 +
-//     2 + 1 + 1 shuffles), after which lane 2m holds row m -- one binary64
-//     accumulator per lane, no per-block conversions.
+//     sums over its 32 lanes with a transpose reduction (the first stage in
+//     binary32, the rest in binary64), after which lane 2m holds row m -- one
+//     binary64 accumulator per lane, no per-block conversions.
 // Generic segments (fields too wide for the fast path) and exceptions take
 // per-lane paths on global memory.
 #ifndef WHFF_P2_STAGES
@@ -274,26 +274,21 @@ __device__ __forceinline__ void pk_band_epilogue(const PkTable& T, const PkJob& 
 #ifndef WHFF_P2_MINB
 #define WHFF_P2_MINB 4
 #endif
-#ifndef WHFF_P2_ITEM
-#define WHFF_P2_ITEM 2
-#endif
 constexpr int kP2Warps = 4;                              // warps per CTA
 constexpr int kP2Split = kPkVW / kP2Warps;               // CTAs per band
 constexpr int kP2Stages = WHFF_P2_STAGES;
-constexpr int kP2ItemTiles = WHFF_P2_ITEM;               // tiles per stage
-#ifdef WHFF_P2_COMPACT
-static_assert(WHFF_P2_ITEM >= 2, "a compact stage holds a 5-word tile only in two tile slots");
-constexpr int kP2TileBytes = 128 * 4 * 4;                // stage tile slot: <= 4 record words
-#else
-constexpr int kP2TileBytes = 128 * pk::kFastWords * 4;   // fast path: <= 5 record words
-#endif
-// tiles per item for a segment of R record words (a 5-word tile needs a
-// whole compact stage)
+// A stage holds the next t tiles of one segment: their records (R words per
+// lane and block-row: R x 512 bytes per tile, contiguous in HBM) followed by
+// their slices of U (512 bytes per tile), t = 12 / (R + 1) capped at a
+// segment -- 2 tiles at R = 4, 5; 3 at R = 3 (most FixedRate(8) segments); 4
+// at R = 2 (FixedAccuracy); 6 at R = 1 -- so the per-item costs (barrier
+// wait, copy issue, cursor) are spread over as many blocks as 6 KB allows.
+constexpr int kP2StageUnits = 12;
+constexpr int kP2StageBytes = kP2StageUnits * 512;
 __device__ __forceinline__ int p2_item_tiles(int R) {
-  return 128 * 4 * R * 1 <= kP2TileBytes ? WHFF_P2_ITEM : 1;
+  const int t = kP2StageUnits / (R + 1);
+  return t < pk::kSegTiles ? t : pk::kSegTiles;
 }
-constexpr int kP2UBytes = kP2ItemTiles * 32 * 16;        // the items' slice of U
-constexpr int kP2StageBytes = kP2ItemTiles * kP2TileBytes + kP2UBytes;
 constexpr int kP2HdrRing = 16;                           // segment headers held per warp
 constexpr int kP2HdrChunk = 8;
 
@@ -824,7 +819,7 @@ __global__ void __launch_bounds__(32 * kP2Warps, WHFF_P2_MINB) k_pk_gemv2(PkTabl
         "@p cp.async.bulk.shared::cluster.global.mbarrier::complete_tx::bytes.L2::cache_hint [%0], [%2], %4, [%1], %7;\n"
         "@p cp.async.bulk.shared::cluster.global.mbarrier::complete_tx::bytes [%8], [%3], %5, [%1];\n"
         "}\n" ::"r"(st), "r"(bar), "l"(pbody), "l"(usrc), "r"(tb), "r"(ub), "r"(tb + ub), "l"(policy),
-        "r"(st + kP2ItemTiles * kP2TileBytes)
+        "r"(st + tb)
         : "memory");
     __syncwarp();   // every lane has read the cursor before lane 0 advances it
     if (lane == 0) {
@@ -907,10 +902,10 @@ __global__ void __launch_bounds__(32 * kP2Warps, WHFF_P2_MINB) k_pk_gemv2(PkTabl
 #pragma unroll 1
           for (int it = 0; it < nt; ++it) {
             if constexpr (kCoef)
-              p2_tile<SPEC>(st + it * twb, st + kP2ItemTiles * kP2TileBytes + it * (pk::kTile * 16), par, m12,
+              p2_tile<SPEC>(st + it * twb, st + nt * twb + it * (pk::kTile * 16), par, m12,
                             k2, hasA, gA, kA, hasB, gB, kB, We, ebase_bits, s);
             else
-              p2_tile_exact<POL, AT>(st + it * twb, st + kP2ItemTiles * kP2TileBytes + it * (pk::kTile * 16),
+              p2_tile_exact<POL, AT>(st + it * twb, st + nt * twb + it * (pk::kTile * 16),
                                      W.par[k & 1], k2, kA, kB, We, (uint32_t)pk::seg_emax_base(S), se);
           }
           // every lane has consumed the stage: refill it with the item kP2Stages ahead
