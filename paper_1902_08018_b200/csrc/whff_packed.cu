@@ -349,42 +349,43 @@ __device__ __forceinline__ pk::FieldPar lds_par_a(uint32_t a) {
   return r;
 }
 
-// The transpose reduction of a segment's 16 per-lane sums over the warp:
-// afterwards lane l holds the sum over the 32 lanes of row m = l >> 1 of the
-// band (m = 4 i + r).  The first stage (xor 16: block-rows 0, 1 against 2, 3)
-// adds binary32 row pairs with FADD2; the rest (xor 8, 4, 2, 1) in AT -- the
-// butterfly restricted to the values each lane keeps.
+// The transpose reduction of a segment's 16 per-lane sums over the warp, in
+// binary32: afterwards lane l holds the sum over the 32 lanes of row m = l >> 1
+// of the band (m = 4 i + r), converted to AT once.  Each stage (xor 16, 8, 4,
+// 2) halves the values a lane keeps -- the butterfly restricted to them --
+// on row pairs with FADD2 while there are pairs; xor 1 finishes.
 template <typename AT>
 __device__ __forceinline__ AT seg_reduce(const float2 s[2][4], int lane) {
   const bool b4 = lane & 16, b3 = lane & 8, b2 = lane & 4, b1 = lane & 2;
-  AT d[8];   // m - 8 b4 = 4 i' + r (i' = row within the kept pair)
+  float2 d[4];   // d[j] = rows (j, 4 + j) of the kept block-row pair: m - 8 b4 = 4 i' + r
 #pragma unroll
   for (int r = 0; r < 4; ++r) {
     const float2 send = b4 ? s[0][r] : s[1][r];
     const float2 mine = b4 ? s[1][r] : s[0][r];
-    const float2 e = __fadd2_rn(mine, make_float2(__shfl_xor_sync(0xFFFFFFFFu, send.x, 16),
-                                                  __shfl_xor_sync(0xFFFFFFFFu, send.y, 16)));
-    d[r] = (AT)e.x;
-    d[4 + r] = (AT)e.y;
+    d[r] = __fadd2_rn(mine, make_float2(__shfl_xor_sync(0xFFFFFFFFu, send.x, 16),
+                                        __shfl_xor_sync(0xFFFFFFFFu, send.y, 16)));
   }
-  AT f[4];
-#pragma unroll
-  for (int j = 0; j < 4; ++j) {
-    const AT send = b3 ? d[j] : d[4 + j];
-    const AT mine = b3 ? d[4 + j] : d[j];
-    f[j] = mine + __shfl_xor_sync(0xFFFFFFFFu, send, 8);
-  }
-  AT g[2];
+  // xor 8: keep i' = b3 (values 4 i' + r, r = 0..3) -> f = rows r = 0..3
+  float2 f[2];
 #pragma unroll
   for (int j = 0; j < 2; ++j) {
-    const AT send = b2 ? f[j] : f[2 + j];
-    const AT mine = b2 ? f[2 + j] : f[j];
-    g[j] = mine + __shfl_xor_sync(0xFFFFFFFFu, send, 4);
+    // (value 2j, value 2j+1) of i' = 0 are d[2j].x, d[2j+1].x; of i' = 1: .y
+    const float2 lo = make_float2(d[2 * j].x, d[2 * j + 1].x), hi = make_float2(d[2 * j].y, d[2 * j + 1].y);
+    const float2 send = b3 ? lo : hi;
+    const float2 mine = b3 ? hi : lo;
+    f[j] = __fadd2_rn(mine, make_float2(__shfl_xor_sync(0xFFFFFFFFu, send.x, 8),
+                                        __shfl_xor_sync(0xFFFFFFFFu, send.y, 8)));
   }
-  const AT send = b1 ? g[0] : g[1];
-  const AT mine = b1 ? g[1] : g[0];
-  AT h = mine + __shfl_xor_sync(0xFFFFFFFFu, send, 2);
-  return h + __shfl_xor_sync(0xFFFFFFFFu, h, 1);
+  // xor 4: keep r in {2 b2, 2 b2 + 1}
+  const float2 send4 = b2 ? f[0] : f[1];
+  const float2 mine4 = b2 ? f[1] : f[0];
+  const float2 g = __fadd2_rn(mine4, make_float2(__shfl_xor_sync(0xFFFFFFFFu, send4.x, 4),
+                                                 __shfl_xor_sync(0xFFFFFFFFu, send4.y, 4)));
+  // xor 2: keep r = 2 b2 + b1
+  const float send2 = b1 ? g.x : g.y;
+  const float mine2 = b1 ? g.y : g.x;
+  const float h = mine2 + __shfl_xor_sync(0xFFFFFFFFu, send2, 2);
+  return (AT)(h + __shfl_xor_sync(0xFFFFFFFFu, h, 1));
 }
 
 // tile-body specialisations (per segment): every group present on its first

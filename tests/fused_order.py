@@ -302,10 +302,10 @@ def packed_model(orc, stream, v, policy="mixed", evaluation="coefficient"):
         R = np.zeros((32, 16), acc_t)                 # [vw, 4 i + r]
         # k_pk_gemv2's order, both evaluations: per segment, per-lane sums over
         # the segment's tiles -- coefficient: binary32 (one FMA rounding per
-        # term), reduced over the warp with a binary32 xor-16 stage and then
-        # xor 8, 4, 2, 1 in binary64; exact: the policy's accumulator (binary64
-        # for mixed), reduced over the warp in it -- accumulated per segment
-        # in the virtual warp's order
+        # term), reduced over the warp in binary32 (xor 16, 8, 4, 2, 1) and
+        # converted once; exact: the policy's accumulator (binary64 for
+        # mixed), reduced over the warp in it -- accumulated per segment in
+        # the virtual warp's order
         Dv_acc = np.zeros((32, 16), acc_t)
         for vw in range(32):
             for sb in range(vw, nsegb, 32):
@@ -323,10 +323,10 @@ def packed_model(orc, stream, v, policy="mixed", evaluation="coefficient"):
                                 for j in range(4):
                                     Se[:, i, r] = np.where(m, Se[:, i, r] + Pa[b, cs, r, j], Se[:, i, r])
                 if evaluation == "coefficient":
-                    # seg_reduce: xor-16 stage in binary32, then xor 8, 4, 2, 1
+                    # seg_reduce: the whole butterfly in binary32, then one
+                    # conversion to the accumulator
                     Dseg = Sg.reshape(32, 16)                          # [lane, m = 4 i + r]
-                    X1 = (Dseg + Dseg[np.arange(32) ^ 16]).astype(np.float32).astype(acc_t)
-                    Dv_acc[vw] = Dv_acc[vw] + _butterfly(np.moveaxis(X1, 0, -1), (8, 4, 2, 1))
+                    Dv_acc[vw] = Dv_acc[vw] + _butterfly(np.moveaxis(Dseg, 0, -1)).astype(acc_t)
                 else:
                     Dv_acc[vw] = Dv_acc[vw] + _butterfly(np.moveaxis(Se.reshape(32, 16), 0, -1))
                 for tt in range(8):
