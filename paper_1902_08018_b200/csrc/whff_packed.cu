@@ -285,10 +285,12 @@ constexpr int kP2Stages = WHFF_P2_STAGES;
 // wait, copy issue, cursor) are spread over as many blocks as 6 KB allows.
 constexpr int kP2StageUnits = 12;
 constexpr int kP2StageBytes = kP2StageUnits * 512;
-__device__ __forceinline__ int p2_item_tiles(int R) {
-  const int t = kP2StageUnits / (R + 1);
-  return t < pk::kSegTiles ? t : pk::kSegTiles;
-}
+// (a nibble table: 12 / (R + 1) for the fast path's R = 1..5, no division)
+constexpr uint32_t kP2ItemTable = 0x22346u;
+static_assert(kP2StageUnits / 2 == 6 && kP2StageUnits / 3 == 4 && kP2StageUnits / 4 == 3 &&
+              kP2StageUnits / 5 == 2 && kP2StageUnits / 6 == 2 && pk::kFastWords == 5,
+              "kP2ItemTable is 12 / (R + 1) for R = 1..5");
+__device__ __forceinline__ int p2_item_tiles(int R) { return (int)((kP2ItemTable >> (4 * (R - 1))) & 15u); }
 constexpr int kP2HdrRing = 16;                           // segment headers held per warp
 constexpr int kP2HdrChunk = 8;
 
@@ -389,9 +391,10 @@ __device__ __forceinline__ AT seg_reduce(const float2 s[2][4], int lane) {
 }
 
 // tile-body specialisations (per segment): every group present on its first
-// candidate pair, groups on the group path (the common rate layout); DC and
-// c = 1, 2 only (the common precision / accuracy layout); anything else
-enum { kSpecFull = 0, kSpecDC = 1, kSpecAny = 2 };
+// candidate pair, groups on the group path (the common rate layout); the same
+// without group B (c = 9..15 all zero: the next most common rate layout); DC
+// and c = 1, 2 only (the common precision / accuracy layout); anything else
+enum { kSpecFull = 0, kSpecDC = 1, kSpecAny = 2, kSpecFullA = 3 };
 
 // One tile of a fast segment from shared memory: adds 2^k (Q u) of the
 // lane's block in each of the four block-rows to s[h][r].
@@ -401,7 +404,7 @@ template <int SPEC>
 __device__ __forceinline__ void p2_tile(uint32_t tw, uint32_t uw, uint32_t par, bool m12, bool k2, bool hasA,
                                         bool gA, bool kA, bool hasB, bool gB, bool kB, int We, uint32_t ebase_bits,
                                         float2 s[2][4]) {
-  constexpr int NW = SPEC == kSpecDC ? 2 : SPEC == kSpecFull ? 4 : pk::kFastWords;   // record words read
+  constexpr int NW = SPEC == kSpecDC ? 2 : SPEC == kSpecFull ? 4 : SPEC == kSpecFullA ? 3 : pk::kFastWords;
   float u[4];
   {
     uint4 t;
@@ -541,10 +544,8 @@ __device__ __forceinline__ void p2_tile(uint32_t tw, uint32_t uw, uint32_t par, 
   using C15_ = std::integral_constant<int, 15>;
   if (SPEC != kSpecAny) {
     run(C1_(), C2_(), I0(), F_(), F_(), T_());
-    if (SPEC == kSpecFull) {
-      run(C3_(), C8_(), I1(), F_(), T_(), F_());
-      run(C9_(), C15_(), I2(), F_(), T_(), F_());
-    }
+    if (SPEC == kSpecFull || SPEC == kSpecFullA) run(C3_(), C8_(), I1(), F_(), T_(), F_());
+    if (SPEC == kSpecFull) run(C9_(), C15_(), I2(), F_(), T_(), F_());
   } else {
     if (m12) run(C1_(), C1_(), I0(), F_(), F_(), T_());
     else run(C1_(), C1_(), I0(), F_(), F_(), F_());
@@ -918,6 +919,7 @@ __global__ void __launch_bounds__(32 * kP2Warps, WHFF_P2_MINB) k_pk_gemv2(PkTabl
       };
       if (!kCoef) items(std::integral_constant<int, kSpecAny>());
       else if (m12 && !k2 && hasA && gA && !kA && hasB && gB && !kB) items(std::integral_constant<int, kSpecFull>());
+      else if (m12 && !k2 && hasA && gA && !kA && !hasB) items(std::integral_constant<int, kSpecFullA>());
       else if (m12 && !k2 && !hasA && !hasB) items(std::integral_constant<int, kSpecDC>());
       else items(std::integral_constant<int, kSpecAny>());
     } else {
