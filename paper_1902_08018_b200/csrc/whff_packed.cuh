@@ -108,6 +108,12 @@ struct Layout {
   int o[16];
 };
 WHFF_HD bool place_group(const int W[16], int c0, int c1, int k, int& cur, int o[16]) {
+  int any = 0;
+  for (int c = c0; c <= c1; ++c) any |= W[c];
+  if (!any) {   // an absent group takes no bits (and does not move the cursor)
+    for (int c = c0; c <= c1; ++c) o[c] = 0;
+    return true;
+  }
   int x = cur < 32 * k ? 32 * k : cur;
   for (int c = c0; c <= c1; ++c) {
     if (W[c] == 0) { o[c] = 0; continue; }
