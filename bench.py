@@ -698,7 +698,11 @@ def b200_main(args, world, rank, local):
         pass
     p50 = statistics.median(lat_ms)
     p99 = sorted(lat_ms)[min(len(lat_ms) - 1, int(0.99 * len(lat_ms)))]
-    launches_per_step = 4 + (1 if args.evaluation == "coefficient" else 0)
+    # source term, 2 CSR products, the fused kernel; the vector prologue
+    # (U = G^T v, or v padded for the packed exact evaluation); the packed
+    # layout's band combine
+    packed = args.layout == "packed"
+    launches_per_step = 4 + (1 if args.evaluation == "coefficient" or packed else 0) + (1 if packed else 0)
     line = {
         "metric": METRIC, "value": round(value, 3), "unit": "GB/s",
         "n_gpus": world, "steps": args.steps, "warmup": args.warmup,
@@ -722,7 +726,7 @@ def b200_main(args, world, rank, local):
                 "ms_per_step": round(e2e_ms, 4), "h2d_bytes_per_step": T * 4,
                 "d2h_bytes_per_step": out_rows * 4},
         "gpu_launches": launches_per_step * args.steps,
-        "roofline": {"bound": "hbm", "kernel": "k_pk_gemv2" if args.layout == "packed" else "k_decode_gemv",
+        "roofline": {"bound": "hbm", "kernel": "k_pk_gemv2 + k_pk_combine" if args.layout == "packed" else "k_decode_gemv",
                      "bytes": ("tile-packed copy read by the launch (body + segment headers + "
                                "exception list) + vector + output" if args.layout == "packed" else
                                "WHFZ payload + device index + vector + output"),

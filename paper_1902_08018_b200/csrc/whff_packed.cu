@@ -142,16 +142,18 @@ __device__ __forceinline__ const PkJob& pk_job(const PkTable& T, uint64_t gband,
   return T.jobs[lo];
 }
 
-// The last of a band's kVW virtual warps to publish its partials combines
-// them (a fixed butterfly per row: the same bits whatever launch computes the
-// band) and writes the band's rows; coefficient evaluation applies the
-// inverse lift G once per block-row here.
-template <int EVAL, int POL, typename AT>
-__device__ __forceinline__ void pk_band_epilogue(const PkTable& T, const PkJob& J, const PkView& P, uint64_t gband,
-                                                 uint64_t band, int nrows, int vw, int lane, const AT* dsum /* [16] per lane: row 4i+r */,
-                                                 bool dsum_lane_major, const AT* rs, unsigned long long* status) {
+// Each of a band's kVW virtual warps publishes its partial record (the
+// per-row sums of its segments, and of its exceptions); k_pk_combine then
+// combines them with a fixed butterfly per row -- the same bits whatever
+// launch (single call, row range, field plan) computes the band -- and
+// coefficient evaluation applies the inverse lift G once per block-row.  The
+// combine is a second kernel (the launch boundary orders the records): the
+// main kernel has no atomics and no memory fences.
+template <int POL, typename AT>
+__device__ __forceinline__ void pk_store_partial(const PkTable& T, uint64_t gband, int vw, int lane,
+                                                 const AT* dsum /* [16] per lane: row 4i+r */, bool dsum_lane_major,
+                                                 const AT* rs) {
   PkRec* grec = T.recs + gband * kVW;
-  unsigned last = 0;
   if (dsum_lane_major) {
     // dsum[0] of lane 2m holds row m (the transpose reduction of k_pk_gemv2)
     if ((lane & 1) == 0) {
@@ -162,7 +164,6 @@ __device__ __forceinline__ void pk_band_epilogue(const PkTable& T, const PkJob& 
       if (POL == WHFF_POLICY_SINGLE) grec[vw].rf[lane] = (float)rs[lane];
       else grec[vw].r[lane] = (double)rs[lane];
     }
-    __syncwarp();
   } else if (lane == 0) {
 #pragma unroll
     for (int k = 0; k < 16; ++k) {
@@ -175,15 +176,11 @@ __device__ __forceinline__ void pk_band_epilogue(const PkTable& T, const PkJob& 
       }
     }
   }
-  if (lane == 0) {
-    unsigned old;
-    asm volatile("atom.acq_rel.gpu.global.inc.u32 %0, [%1], %2;"
-                 : "=r"(old) : "l"(T.tickets + gband), "r"(kVW - 1u) : "memory");
-    last = old == kVW - 1u;
-  }
-  if (!__shfl_sync(0xFFFFFFFFu, last, 0)) return;
-  __syncwarp();
-  asm volatile("fence.acq_rel.gpu;" ::: "memory");
+}
+
+template <int EVAL, int POL, typename AT>
+__device__ __forceinline__ void pk_combine_band(const PkJob& J, const PkView& P, const PkRec* grec, uint64_t band,
+                                                int nrows, int lane, unsigned long long* status) {
   // lane = virtual warp: 32 records, fixed butterfly per row
   AT D[16], R[16];
 #pragma unroll
@@ -979,8 +976,21 @@ __global__ void __launch_bounds__(32 * kP2Warps, WHFF_P2_MINB) k_pk_gemv2(PkTabl
     if (S.exc_count) pk_exceptions<POL, AT>(J.p, J.v, band, S.exc_begin, S.exc_count, lane, W.rs);
   }
   asm volatile("cp.async.wait_group 0;" ::: "memory");
-  pk_band_epilogue<EVAL, POL, AT>(T, J, J.p, gband, band, pk::band_rows(J.p.g, band), vw, lane, &acc, true, W.rs,
-                                  status);
+  __syncwarp();
+  pk_store_partial<POL, AT>(T, gband, vw, lane, &acc, true, W.rs);
+}
+
+// one warp per band: the band's 32 partial records -> its rows of y
+template <int EVAL, int POL>
+__global__ void __launch_bounds__(128) k_pk_combine(PkTable T, unsigned long long* status) {
+  using AT = typename PkAcc<POL>::T;
+  const uint64_t gband = (uint64_t)blockIdx.x * 4 + (threadIdx.x >> 5);
+  if (gband >= T.total_bands) return;
+  const int lane = threadIdx.x & 31;
+  uint64_t first;
+  const PkJob& J = pk_job(T, gband, first);
+  const uint64_t band = J.band0 + (gband - first);
+  pk_combine_band<EVAL, POL, AT>(J, J.p, T.recs + gband * kVW, band, pk::band_rows(J.p.g, band), lane, status);
 }
 
 template <int EVAL, int POL>
@@ -992,6 +1002,7 @@ static cudaError_t p2_launch(const PkTable& T, unsigned long long* status, cudaS
   if (e != cudaSuccess) return e;
   const unsigned blocks = (unsigned)(T.total_bands * kP2Split);
   k_pk_gemv2<EVAL, POL><<<blocks, 32 * kP2Warps, smem, cs>>>(T, status);
+  k_pk_combine<EVAL, POL><<<(unsigned)((T.total_bands + 3) / 4), 128, 0, cs>>>(T, status);
   return cudaGetLastError();
 }
 
