@@ -298,13 +298,15 @@ struct alignas(16) P2Ctl {
   uint64_t pbody, usrc;                  // next item: body and U source addresses
   uint32_t pk, pt, pntl, pslot;          // producer cursor: segment, tile, its tiles, stage
   uint32_t ptw, nseg, hdr_loaded, ntile; // words per tile of segment pk; warp constants
+  uint32_t hdr_landed, pad0, pad1, pad2;  // header ring: slots known to have landed
   uint64_t body, U, gsegs, gpars, policy, pad;
 };
 template <typename AT>
 struct alignas(128) P2Warp {
   uint8_t stage[kP2Stages][kP2StageBytes];
   uint64_t bar[kP2Stages];
-  pk::Seg seg[kP2HdrRing];
+  pk::Seg seg[kP2HdrRing];     // the producer's header ring
+  pk::Seg cur[2];              // the consumer's: this segment's and the next one's (cp.async prefetch)
   pk::FieldPar par[2][16];     // this segment's and the next one's (cp.async prefetch)
   AT rs[16];
   P2Ctl ctl;
@@ -709,7 +711,7 @@ __global__ void __launch_bounds__(32 * kP2Warps, WHFF_P2_MINB) k_pk_gemv2(PkTabl
   const uint32_t c_pk = ctl + offsetof(P2Ctl, pk), c_pt = ctl + offsetof(P2Ctl, pt);
   const uint32_t c_pslot = ctl + offsetof(P2Ctl, pslot), c_pntl = ctl + offsetof(P2Ctl, pntl);
   const uint32_t c_nseg = ctl + offsetof(P2Ctl, nseg), c_hdr = ctl + offsetof(P2Ctl, hdr_loaded);
-  const uint32_t c_ntile = ctl + offsetof(P2Ctl, ntile);
+  const uint32_t c_ntile = ctl + offsetof(P2Ctl, ntile), c_landed = ctl + offsetof(P2Ctl, hdr_landed);
   {
     const PkView& P = J.p;
     const uint64_t nsegb = P.g.nsegb;
@@ -727,6 +729,7 @@ __global__ void __launch_bounds__(32 * kP2Warps, WHFF_P2_MINB) k_pk_gemv2(PkTabl
       ctl_st32(c_pslot, 0);
       ctl_st32(c_nseg, (uint32_t)nseg);
       ctl_st32(c_hdr, 0);
+      ctl_st32(c_landed, 0);
       ctl_st32(c_ntile, (uint32_t)P.g.ntile);
     }
     if (lane < 16) W.rs[lane] = (AT)0;
@@ -738,22 +741,44 @@ __global__ void __launch_bounds__(32 * kP2Warps, WHFF_P2_MINB) k_pk_gemv2(PkTabl
     __syncwarp();
   }
 
-  // segment headers -> a shared-memory ring, kP2HdrChunk at a time (the
-  // producer runs at most kP2Stages items -- so at most kP2Stages segments --
-  // ahead of the consumer: a header is never overwritten while needed)
-  static_assert(kP2HdrRing - kP2HdrChunk > kP2Stages, "header ring too small");
-  auto ensure_hdr = [&](int k) {
-    int loaded = (int)ctl_ld32(c_hdr);
-    if (k < loaded) return;
-    const pk::Seg* gsegs = reinterpret_cast<const pk::Seg*>(ctl_ld64(c_gsegs));
+  // Segment headers.  The producer walks them forward through a
+  // shared-memory ring, kP2HdrChunk at a time; only it reads the ring, so a
+  // chunk may overwrite any slot behind its cursor (however many generic
+  // segments it skips).  Each chunk is copied with cp.async; when the
+  // producer enters chunk c it also starts chunk c + 1, which it then finds
+  // landed (a cp.async.wait_group makes sure).  The consumer reads its own
+  // copy of each header (W.cur), prefetched one segment ahead like the
+  // parameters.
+  static_assert(kP2HdrRing == 2 * kP2HdrChunk, "the header ring holds two chunks");
+  auto hdr_chunk = [&](int c) {   // cp.async chunk c into the ring (lanes 0..23: 3 x 16 bytes each)
     const int nseg = (int)ctl_ld32(c_nseg);
-    while (k >= loaded) {
-      const int kk = loaded + lane;
-      if (lane < kP2HdrChunk && kk < nseg) W.seg[kk & (kP2HdrRing - 1)] = gsegs[(uint64_t)kVW * kk];
-      loaded += kP2HdrChunk;
+    const int kk = c * kP2HdrChunk + lane / 3;
+    if (lane < 3 * kP2HdrChunk && kk < nseg) {
+      const char* g = reinterpret_cast<const char*>(reinterpret_cast<const pk::Seg*>(ctl_ld64(c_gsegs)) +
+                                                    (uint64_t)kVW * kk) + 16 * (lane % 3);
+      asm volatile("cp.async.cg.shared.global [%0], [%1], 16;"
+                   ::"r"(smem_addr(&W.seg[kk & (kP2HdrRing - 1)]) + 16 * (lane % 3)), "l"(g) : "memory");
     }
+    asm volatile("cp.async.commit_group;" ::: "memory");
+  };
+  auto ensure_hdr = [&](int k) {
+    if (k < (int)ctl_ld32(c_landed)) return;
+    int loaded = (int)ctl_ld32(c_hdr);
+    if (k >= loaded) {                       // chunk(s) never started: start up to k's
+      while (k >= loaded) {
+        hdr_chunk(loaded / kP2HdrChunk);
+        loaded += kP2HdrChunk;
+      }
+    }
+    asm volatile("cp.async.wait_group 0;" ::: "memory");
     __syncwarp();
-    if (lane == 0) ctl_st32(c_hdr, (uint32_t)loaded);
+    const int landed = loaded;
+    hdr_chunk(loaded / kP2HdrChunk);         // and the next chunk, in the background
+    loaded += kP2HdrChunk;
+    if (lane == 0) {
+      ctl_st32(c_hdr, (uint32_t)loaded);
+      ctl_st32(c_landed, (uint32_t)landed);
+    }
     __syncwarp();
   };
   auto hdr = [&](int k) -> const pk::Seg& { return W.seg[k & (kP2HdrRing - 1)]; };
@@ -832,12 +857,20 @@ __global__ void __launch_bounds__(32 * kP2Warps, WHFF_P2_MINB) k_pk_gemv2(PkTabl
   skip(0, 0);
   for (int i = 0; i < kP2Stages; ++i) issue();
 
-  // parameters of the warp's segment k -> par[k & 1] (cp.async: no registers)
+  // header and parameters of the warp's segment k -> cur[k & 1], par[k & 1]
+  // (cp.async: no registers)
   auto prefetch_par = [&](int k) {
-    if (kCoef && lane < 16 && k < (int)ctl_ld32(c_nseg)) {
-      const pk::FieldPar* gp = reinterpret_cast<const pk::FieldPar*>(ctl_ld64(c_gpars));
-      asm volatile("cp.async.cg.shared.global [%0], [%1], 16;" ::"r"(par0 + 256 * (k & 1) + 16 * lane),
-                   "l"(gp + (uint64_t)kVW * 16 * k + lane) : "memory");
+    if (k < (int)ctl_ld32(c_nseg)) {
+      if (kCoef && lane < 16) {
+        const pk::FieldPar* gp = reinterpret_cast<const pk::FieldPar*>(ctl_ld64(c_gpars));
+        asm volatile("cp.async.cg.shared.global [%0], [%1], 16;" ::"r"(par0 + 256 * (k & 1) + 16 * lane),
+                     "l"(gp + (uint64_t)kVW * 16 * k + lane) : "memory");
+      } else if (lane >= 16 && lane < 19) {
+        const char* g = reinterpret_cast<const char*>(reinterpret_cast<const pk::Seg*>(ctl_ld64(c_gsegs)) +
+                                                      (uint64_t)kVW * k) + 16 * (lane - 16);
+        asm volatile("cp.async.cg.shared.global [%0], [%1], 16;"
+                     ::"r"(smem_addr(&W.cur[k & 1]) + 16 * (lane - 16)), "l"(g) : "memory");
+      }
     }
     asm volatile("cp.async.commit_group;" ::: "memory");
   };
@@ -849,16 +882,15 @@ __global__ void __launch_bounds__(32 * kP2Warps, WHFF_P2_MINB) k_pk_gemv2(PkTabl
   const int nseg = (int)ctl_ld32(c_nseg);
 
   for (int k = 0; k < nseg; ++k) {
-    ensure_hdr(k);
-    const pk::Seg& S = hdr(k);   // shared memory
+    // this segment's header and parameters have landed; start the next one's
+    asm volatile("cp.async.wait_group 0;" ::: "memory");
+    __syncwarp();
+    prefetch_par(k + 1);
+    const pk::Seg& S = W.cur[k & 1];   // shared memory
     const int L = pk::seg_L(S);
     const int We = pk::seg_We(S);
     const int ntl = seg_ntl(k);
     const uint32_t ebase_bits = ((uint32_t)pk::seg_emax_base(S) - 59u) << 23;   // binary32 2^(emax_base - 186)
-    // this segment's parameters have landed; start the next one's
-    asm volatile("cp.async.wait_group 0;" ::: "memory");
-    __syncwarp();
-    prefetch_par(k + 1);
     const uint32_t par = par0 + 256 * (k & 1);
     // the segment's per-lane sums: coefficient, binary32 s[h][r] = (block-row
     // 2h, 2h + 1) x row r; exact, AT se[4 i + r]
@@ -935,7 +967,7 @@ __global__ void __launch_bounds__(32 * kP2Warps, WHFF_P2_MINB) k_pk_gemv2(PkTabl
           if (i >= pk::band_rows(P.g, band)) break;
           int32_t q[16];
           uint32_t ed;
-          pk_generic_parse(&hdr(k), sbody + tt * TW, lane, i, q, &ed);
+          pk_generic_parse(&S, sbody + tt * TW, lane, i, q, &ed);
           if constexpr (!kCoef) {
             // (u holds v here: the exact evaluation's padded vector slice)
             float x[16];

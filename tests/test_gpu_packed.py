@@ -246,3 +246,23 @@ def test_staged_kernel_wide_bands(orc, policy, rng):
     got = _packed_gemv(s, v, policy, "coefficient")
     want = packed_model(orc, s, v, policy, "coefficient")
     assert np.array_equal(got.view(np.uint32), want.view(np.uint32))
+
+
+@pytest.mark.parametrize("evaluation", ["coefficient", "exact"])
+def test_staged_kernel_runs_of_generic_segments(orc, evaluation, rng):
+    """Long runs of generic segments (random data at a high rate: fields too
+    wide for the fast path) between fast ones: the producer skips far ahead
+    of the consumer through the header ring.  Every virtual warp sees a fast
+    segment, 18 generic ones, then fast ones again; bit-exact vs the model."""
+    from fused_order import packed_model
+    from paper_1902_08018_b200 import codec
+    seg_cols, vws = 1024, 32
+    cols = 20 * vws * seg_cols
+    C0 = smooth_matrix(6, cols, S=cols)
+    wild = rng.standard_normal((6, 18 * vws * seg_cols)).astype(np.float32) * np.float32(1e-8)
+    C0[:, vws * seg_cols:19 * vws * seg_cols] = wild
+    s = codec.compress(C0, codec.FixedRate(24))
+    v = rng.random(cols).astype(np.float32)
+    got = _packed_gemv(s, v, "mixed", evaluation)
+    want = packed_model(orc, s, v, "mixed", evaluation)
+    assert np.array_equal(got.view(np.uint32), want.view(np.uint32))
