@@ -280,13 +280,22 @@ constexpr int kP2Stages = WHFF_P2_STAGES;
 // segment -- 2 tiles at R = 4, 5; 3 at R = 3 (most FixedRate(8) segments); 4
 // at R = 2 (FixedAccuracy); 6 at R = 1 -- so the per-item costs (barrier
 // wait, copy issue, cursor) are spread over as many blocks as 6 KB allows.
-constexpr int kP2StageUnits = 12;
+#ifndef WHFF_P2_UNITS
+#define WHFF_P2_UNITS 12
+#endif
+constexpr int kP2StageUnits = WHFF_P2_UNITS;
 constexpr int kP2StageBytes = kP2StageUnits * 512;
-// (a nibble table: 12 / (R + 1) for the fast path's R = 1..5, no division)
-constexpr uint32_t kP2ItemTable = 0x22346u;
-static_assert(kP2StageUnits / 2 == 6 && kP2StageUnits / 3 == 4 && kP2StageUnits / 4 == 3 &&
-              kP2StageUnits / 5 == 2 && kP2StageUnits / 6 == 2 && pk::kFastWords == 5,
-              "kP2ItemTable is 12 / (R + 1) for R = 1..5");
+// (a nibble table: min(8, units / (R + 1)) for the fast path's R = 1..5, no division)
+constexpr uint32_t p2_item_table(int units) {
+  uint32_t t = 0;
+  for (int R = 1; R <= 5; ++R) {
+    const int n = units / (R + 1) < pk::kSegTiles ? units / (R + 1) : pk::kSegTiles;
+    t |= (uint32_t)n << (4 * (R - 1));
+  }
+  return t;
+}
+constexpr uint32_t kP2ItemTable = p2_item_table(kP2StageUnits);
+static_assert(pk::kFastWords == 5 && kP2StageUnits >= 6, "every fast-path record fits one tile per stage");
 __device__ __forceinline__ int p2_item_tiles(int R) { return (int)((kP2ItemTable >> (4 * (R - 1))) & 15u); }
 constexpr int kP2HdrRing = 16;                           // segment headers held per warp
 constexpr int kP2HdrChunk = 8;
