@@ -48,6 +48,7 @@ __device__ __forceinline__ pk::FieldPar lds_par(const pk::FieldPar* p) {
 
 // All 16 coefficients (sequency order) of one fast-path record (decode-only
 // and exact evaluation; the pair of each group is selected per segment).
+template <bool HASA = true, bool HASB = true>
 __device__ __forceinline__ void pk_fields_int(const uint32_t a[pk::kFastWords], const pk::FieldPar* par /* smem */,
                                               bool k2, bool kA, bool kB, int32_t q[16]) {
   q[0] = pk::field_dc(a[0], a[1], lds_par(par));
@@ -56,9 +57,9 @@ __device__ __forceinline__ void pk_fields_int(const uint32_t a[pk::kFastWords], 
   const uint32_t hA = kA ? a[2] : a[1], lA = kA ? a[3] : a[2];
   const uint32_t hB = kB ? a[3] : a[2], lB = kB ? a[4] : a[3];
 #pragma unroll
-  for (int c = 3; c <= 8; ++c) q[c] = pk::field_i(hA, lA, lds_par(par + c));
+  for (int c = 3; c <= 8; ++c) q[c] = HASA ? pk::field_i(hA, lA, lds_par(par + c)) : 0;
 #pragma unroll
-  for (int c = 9; c < 16; ++c) q[c] = pk::field_i(hB, lB, lds_par(par + c));
+  for (int c = 9; c < 16; ++c) q[c] = HASB ? pk::field_i(hB, lB, lds_par(par + c)) : 0;
 }
 
 // Generic path: the whole record (any L) of (row i, lane) into rec[].
@@ -628,7 +629,9 @@ __device__ __forceinline__ AT seg_reduce16(const AT d[16], int lane) {
 // dequantisation, codec.py:128-218), times v in the policy's arithmetic,
 // added to se[4 i + r] in (row, column) order.
 // tw: stage address of the lane's first record word; vwa: of its v entry.
-template <int POL, typename AT>
+// HASA / HASB: coefficient groups 3..8 / 9..15 present in the segment (an
+// absent group is all zeros: its fields are not read and the lift folds them).
+template <int POL, typename AT, bool HASA, bool HASB>
 __device__ __forceinline__ void p2_tile_exact(uint32_t tw, uint32_t vwa, const pk::FieldPar* par, bool k2, bool kA,
                                               bool kB, int We, uint32_t ebase, AT se[16]) {
   float v[4];
@@ -647,7 +650,7 @@ __device__ __forceinline__ void p2_tile_exact(uint32_t tw, uint32_t vwa, const p
     for (int kw = 0; kw < pk::kFastWords; ++kw)
       asm volatile("ld.shared.u32 %0, [%1];" : "=r"(a[kw]) : "r"(tw + 512 * kw + 4 * i));
     int32_t q[16], t[16];
-    pk_fields_int(a, par, k2, kA, kB, q);
+    pk_fields_int<HASA, HASB>(a, par, k2, kA, kB, q);
     lift_signed(q, t);
     // dequantisation (codec.py:201-206) on the packed pipe when the scale
     // is a normal-or-subnormal binary32 power of two (single rounding,
@@ -944,9 +947,15 @@ __global__ void __launch_bounds__(32 * kP2Warps, WHFF_P2_MINB) k_pk_gemv2(PkTabl
             if constexpr (kCoef)
               p2_tile<SPEC>(st + it * twb, st + nt * twb + it * (pk::kTile * 16), par, m12,
                             k2, hasA, gA, kA, hasB, gB, kB, We, ebase_bits, s);
+            else if (SPEC == kSpecDC)
+              p2_tile_exact<POL, AT, false, false>(st + it * twb, st + nt * twb + it * (pk::kTile * 16),
+                                                   W.par[k & 1], k2, kA, kB, We, (uint32_t)pk::seg_emax_base(S), se);
+            else if (SPEC == kSpecFullA)
+              p2_tile_exact<POL, AT, true, false>(st + it * twb, st + nt * twb + it * (pk::kTile * 16),
+                                                  W.par[k & 1], k2, kA, kB, We, (uint32_t)pk::seg_emax_base(S), se);
             else
-              p2_tile_exact<POL, AT>(st + it * twb, st + nt * twb + it * (pk::kTile * 16),
-                                     W.par[k & 1], k2, kA, kB, We, (uint32_t)pk::seg_emax_base(S), se);
+              p2_tile_exact<POL, AT, true, true>(st + it * twb, st + nt * twb + it * (pk::kTile * 16),
+                                                 W.par[k & 1], k2, kA, kB, We, (uint32_t)pk::seg_emax_base(S), se);
           }
           // every lane has consumed the stage: refill it with the item kP2Stages ahead
           __syncwarp();
@@ -955,7 +964,13 @@ __global__ void __launch_bounds__(32 * kP2Warps, WHFF_P2_MINB) k_pk_gemv2(PkTabl
           cphase ^= cslot == 0 ? 1u : 0u;
         }
       };
-      if (!kCoef) items(std::integral_constant<int, kSpecAny>());
+      // exact evaluation: the body for the groups present (kSpecDC: no
+      // groups, kSpecFullA: group A only, kSpecAny: both)
+      if (!kCoef) {
+        if (!hasA && !hasB) items(std::integral_constant<int, kSpecDC>());
+        else if (!hasB) items(std::integral_constant<int, kSpecFullA>());
+        else items(std::integral_constant<int, kSpecAny>());
+      }
       else if (m12 && !k2 && hasA && gA && !kA && hasB && gB && !kB) items(std::integral_constant<int, kSpecFull>());
       else if (m12 && !k2 && hasA && gA && !kA && !hasB) items(std::integral_constant<int, kSpecFullA>());
       else if (m12 && !k2 && !hasA && !hasB) items(std::integral_constant<int, kSpecDC>());
