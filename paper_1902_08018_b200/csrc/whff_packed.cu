@@ -182,39 +182,31 @@ __device__ __forceinline__ void pk_store_partial(const PkTable& T, uint64_t gban
 template <int EVAL, int POL, typename AT>
 __device__ __forceinline__ void pk_combine_band(const PkJob& J, const PkView& P, const PkRec* grec, uint64_t band,
                                                 int nrows, int lane, unsigned long long* status) {
-  // lane = virtual warp: 32 records, fixed butterfly per row
-  AT D[16], R[16];
+  // lane = value (0..15: the block sums D of row lane, 16..31: the exception
+  // sums R of row lane - 16), read from the 32 records (coalesced: one
+  // 128-byte line per record and kind), then summed over the records in the
+  // fixed xor-butterfly order (16, 8, 4, 2, 1) -- the pairwise tree that
+  // leaves the same bits in every lane of a shuffle butterfly.
+  AT x[kVW];
 #pragma unroll
-  for (int k = 0; k < 16; ++k) {
-    if (POL == WHFF_POLICY_SINGLE) {
-      D[k] = (AT)__ldcg(&grec[lane].f[k]);
-      R[k] = (AT)__ldcg(&grec[lane].rf[k]);
-    } else {
-      D[k] = (AT)__ldcg(&grec[lane].d[k]);
-      R[k] = (AT)__ldcg(&grec[lane].r[k]);
-    }
+  for (int w = 0; w < kVW; ++w) {
+    if (POL == WHFF_POLICY_SINGLE) x[w] = (AT)__ldcg(lane < 16 ? &grec[w].f[lane] : &grec[w].rf[lane - 16]);
+    else x[w] = (AT)__ldcg(lane < 16 ? &grec[w].d[lane] : &grec[w].r[lane - 16]);
   }
 #pragma unroll
-  for (int o = 16; o > 0; o >>= 1)
+  for (int o = kVW / 2; o > 0; o >>= 1)
 #pragma unroll
-    for (int k = 0; k < 16; ++k) {
-      D[k] = D[k] + __shfl_xor_sync(0xFFFFFFFFu, D[k], o);
-      R[k] = R[k] + __shfl_xor_sync(0xFFFFFFFFu, R[k], o);
-    }
+    for (int w = 0; w < o; ++w) x[w] = x[w] + x[w + o];
+  const AT tot = x[0];
+  // row m = lane (< 16) of the band: its R and the D of the block-row's 4 rows
+  const int i = (lane >> 2) & 3, rr = lane & 3;
+  const AT rsel = __shfl_sync(0xFFFFFFFFu, tot, 16 + (lane & 15));
+  const AT d0 = __shfl_sync(0xFFFFFFFFu, tot, 4 * i + 0), d1 = __shfl_sync(0xFFFFFFFFu, tot, 4 * i + 1);
+  const AT d2 = __shfl_sync(0xFFFFFFFFu, tot, 4 * i + 2), d3 = __shfl_sync(0xFFFFFFFFu, tot, 4 * i + 3);
   if (lane < 16) {
-    const int i = lane >> 2, rr = lane & 3;
     const uint64_t row = (band * pk::kBand + i) * 4 + rr;
     if (i < nrows && row >= J.row_begin && row < J.row_end && row < P.g.rows) {
       float out;
-      AT rsel = R[0], d0 = D[0], d1 = D[1], d2 = D[2], d3 = D[3], dsel = D[0];
-#pragma unroll
-      for (int k = 0; k < 16; ++k) {
-        if (k == lane) { rsel = R[k]; dsel = D[k]; }
-        if (k == 4 * i + 0) d0 = D[k];
-        if (k == 4 * i + 1) d1 = D[k];
-        if (k == 4 * i + 2) d2 = D[k];
-        if (k == 4 * i + 3) d3 = D[k];
-      }
       if (EVAL == WHFF_EVAL_COEFF) {
         const AT dd[4] = {d0, d1, d2, d3};
         if (POL == WHFF_POLICY_SINGLE) {
@@ -229,8 +221,8 @@ __device__ __forceinline__ void pk_combine_band(const PkJob& J, const PkView& P,
           out = __double2float_rn(t);
         }
       } else {
-        if (POL == WHFF_POLICY_SINGLE) out = __fadd_rn((float)dsel, (float)rsel);
-        else out = __double2float_rn(__dadd_rn((double)dsel, (double)rsel));
+        if (POL == WHFF_POLICY_SINGLE) out = __fadd_rn((float)tot, (float)rsel);
+        else out = __double2float_rn(__dadd_rn((double)tot, (double)rsel));
       }
       J.y[row - J.row_begin] = out;
       if (!isfinite(out)) atomicMin(status, (unsigned long long)row);
