@@ -635,7 +635,15 @@ __device__ __forceinline__ void p2_tile_exact(uint32_t tw, uint32_t vwa, const p
     v[2] = __uint_as_float(t.z);
     v[3] = __uint_as_float(t.w);
   }
+  // The four block-rows, one loop trip each (not unrolled: the body is
+  // long).  se[] is indexed statically: each trip works on se[0..3] and
+  // rotates the array by one block-row, so after four trips every sum is
+  // back in place (a dynamic index would put se[] in local memory).
+#if WHFF_EXACT_UNROLL
+#pragma unroll
+#else
 #pragma unroll 1
+#endif
   for (int i = 0; i < 4; ++i) {
     uint32_t a[pk::kFastWords];
 #pragma unroll
@@ -663,7 +671,7 @@ __device__ __forceinline__ void p2_tile_exact(uint32_t tw, uint32_t vwa, const p
     }
 #pragma unroll
     for (int r = 0; r < 4; ++r) {
-      AT acc = se[4 * i + r];
+      AT acc = se[r];
       if (POL == WHFF_POLICY_DOUBLE) {
 #pragma unroll
         for (int j = 0; j < 4; ++j) acc = __dadd_rn(acc, __dmul_rn((double)x[4 * r + j], (double)v[j]));
@@ -681,8 +689,13 @@ __device__ __forceinline__ void p2_tile_exact(uint32_t tw, uint32_t vwa, const p
           }
         }
       }
-      se[4 * i + r] = acc;
+      se[r] = acc;
     }
+    AT rot[16];   // rotate by one block-row (a register permutation)
+#pragma unroll
+    for (int m = 0; m < 16; ++m) rot[m] = se[(m + 4) & 15];
+#pragma unroll
+    for (int m = 0; m < 16; ++m) se[m] = rot[m];
   }
 }
 
