@@ -1104,8 +1104,25 @@ __global__ void k_csr_matvec(const int64_t* indptr, const int32_t* indices, cons
   if (i >= n) return;
   double acc = 0.0;
   const int64_t e = indptr[i + 1];
-  for (int64_t jj = indptr[i]; jj < e; ++jj)
-    acc = __dadd_rn(acc, __dmul_rn(ldg(data + jj), (double)ldg(x + ldg(indices + jj))));
+  // eight entries at a time: their loads and gathers are issued together
+  // (two memory round trips per eight instead of two per entry); the sum
+  // stays in the row's order (scipy's)
+  for (int64_t b = indptr[i]; b < e; b += 8) {
+    double d[8];
+    float xv[8];
+#pragma unroll
+    for (int k = 0; k < 8; ++k) {
+      d[k] = 0.0;
+      xv[k] = 0.0f;
+      if (b + k < e) {
+        d[k] = ldg(data + b + k);
+        xv[k] = ldg(x + ldg(indices + b + k));
+      }
+    }
+#pragma unroll
+    for (int k = 0; k < 8; ++k)
+      if (b + k < e) acc = __dadd_rn(acc, __dmul_rn(d[k], (double)xv[k]));
+  }
   if (bdiag != nullptr) acc = __dadd_rn(acc, __dmul_rn((double)bdiag[i], (double)u[i]));
   y[i] = __double2float_rn(acc);
 }
