@@ -243,8 +243,8 @@ whff_status_t whff_decode(whff_dstream_t s, float* out_dev, uint64_t ld_out,
 /* y[r - row_begin] = sum_j C[r, j] * v[j] for r in [row_begin, row_end),
  * C the decoded stream.  v_dev has `cols` floats, y_dev row_end-row_begin.
  * workspace: whff_decode_gemv_workspace_size bytes of device memory, 16-byte
- * aligned, any contents (the per-row partial sums and arrival counters; for
- * the coefficient evaluation also G^T v).  A row's result does not depend on
+ * aligned, any contents (the per-band partial sums; the stream layouts also
+ * keep arrival counters there; the coefficient evaluation also G^T v).  A row's result does not depend on
  * the row range or on batching (plans give the same bits).  Calls sharing a
  * workspace must be ordered (one stream).                                  */
 whff_status_t whff_decode_gemv_workspace_size(whff_dstream_t s, int eval, size_t* bytes);

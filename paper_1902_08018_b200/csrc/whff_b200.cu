@@ -2122,7 +2122,7 @@ static uint64_t ws_pkrec_bytes(const whff_dstream* s) { return align256(pk_nband
 extern "C" whff_status_t whff_decode_gemv_workspace_size(whff_dstream_t s, int eval, size_t* bytes) {
   if (!s || !bytes) return fail(WHFF_ERR_ARGUMENT, "null argument");
   if (s->packed)
-    *bytes = ws_u_bytes(s, eval) + ws_pkrec_bytes(s) + pk_nband(s) * sizeof(unsigned);
+    *bytes = ws_u_bytes(s, eval) + ws_pkrec_bytes(s);
   else
     *bytes = ws_u_bytes(s, eval) + ws_rec_bytes(s) + std::max<uint64_t>(s->br, 1) * sizeof(unsigned);
   return WHFF_OK;
@@ -2174,9 +2174,6 @@ extern "C" whff_status_t whff_decode_gemv(whff_dstream_t s, const float* v, floa
     if ((reinterpret_cast<uintptr_t>(ws) & 15u) != 0) return fail(WHFF_ERR_ARGUMENT, "workspace alignment");
     uint8_t* wsb = reinterpret_cast<uint8_t*>(ws);
     T.recs = reinterpret_cast<PkRec*>(wsb + ws_u_bytes(s, eval));
-    T.tickets = reinterpret_cast<unsigned*>(wsb + ws_u_bytes(s, eval) + ws_pkrec_bytes(s));
-    cudaError_t me = cudaMemsetAsync(T.tickets, 0, T.total_bands * sizeof(unsigned), cs);
-    if (me != cudaSuccess) return cuda_fail(me, "workspace clear");
     vec_prologue(eval, v, s->cols, s->bc, reinterpret_cast<float4*>(ws), cs);
     WCK_LAUNCH("vector prologue");
     T.single.U = reinterpret_cast<const float4*>(ws);
@@ -2304,14 +2301,11 @@ static whff_status_t plan_create_packed(int n, const whff_dstream_t* streams, co
   if (e == cudaSuccess) e = cudaMemcpy(P->d_pkjobs, jobs.data(), n * sizeof(PkJob), cudaMemcpyHostToDevice);
   if (e == cudaSuccess) e = cudaMemcpy(P->d_prefix, prefix.data(), n * 8, cudaMemcpyHostToDevice);
   if (e == cudaSuccess) e = cudaMalloc(&P->d_pkrecs, std::max<uint64_t>(bands, 1) * kPkVW * sizeof(PkRec));
-  if (e == cudaSuccess) e = cudaMalloc(&P->d_tickets, std::max<uint64_t>(bands, 1) * sizeof(unsigned));
-  if (e == cudaSuccess) e = cudaMemset(P->d_tickets, 0, std::max<uint64_t>(bands, 1) * sizeof(unsigned));
   if (e != cudaSuccess) {
     cudaFree(P->d_U);
     cudaFree(P->d_pkjobs);
     cudaFree(P->d_prefix);
     cudaFree(P->d_pkrecs);
-    cudaFree(P->d_tickets);
     delete P;
     return cuda_fail(e, "plan create (packed)");
   }
@@ -2442,7 +2436,6 @@ whff_status_t whff_gemv_plan_launch(whff_gemv_plan_t P, uint64_t* status, whff_s
     T.max_nsegb = P->pk_max_nsegb;
     memset(&T.single, 0, sizeof(T.single));
     T.recs = P->d_pkrecs;
-    T.tickets = P->d_tickets;
     return launch_pk(P->eval, P->policy, T, reinterpret_cast<unsigned long long*>(status), cs);
   }
   JobTable T;

@@ -44,8 +44,7 @@ struct PkTable {
   uint64_t total_bands;
   uint64_t max_nsegb;        // widest band of any job, in segments (kernel choice)
   PkJob single;
-  PkRec* recs;               // [band][kVW]
-  unsigned* tickets;         // [band] (zero between launches)
+  PkRec* recs;               // [band][kVW] partial records (k_pk_gemv2 -> k_pk_combine)
 };
 
 
