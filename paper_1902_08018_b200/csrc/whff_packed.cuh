@@ -14,7 +14,7 @@
 //   band     = 4 block-rows (16 matrix rows)
 //   tile     = band x 32 block-columns; lane l of a warp owns block-column
 //              32 t + l of every block-row of the band
-//   segment  = band x up to 8 tiles (256 block-columns) sharing one "field
+//   segment  = band x up to 16 tiles (512 block-columns) sharing one "field
 //              profile": a width W_c per coefficient c (sequency order,
 //              codec.py:40) = the widest value of c in the segment, and a
 //              width W_e for emax - emax_base
@@ -57,7 +57,10 @@ namespace pk {
 
 constexpr int kBand = 4;          // block-rows per band
 constexpr int kTile = 32;         // block-columns per tile (one per lane)
-constexpr int kSegTiles = 8;      // tiles per segment
+#ifndef WHFF_SEG_TILES
+#define WHFF_SEG_TILES 16
+#endif
+constexpr int kSegTiles = WHFF_SEG_TILES;   // tiles per segment (tests/fused_order.py SEG_TILES)
 constexpr int kSegCols = kTile * kSegTiles;
 constexpr int kMagicW = 23;       // widest offset-binary field on the magic path
 constexpr int kMaxRecordBits = 9 + 28 * 16;
@@ -192,7 +195,7 @@ struct Geom {
   uint64_t rows, cols, br, bc;
   uint64_t nband;   // ceil(br / 4)
   uint64_t ntile;   // tiles per band: ceil(bc / 32)
-  uint64_t nsegb;   // segments per band: ceil(ntile / 8)
+  uint64_t nsegb;   // segments per band: ceil(ntile / kSegTiles)
 };
 WHFF_HD Geom make_geom(uint64_t rows, uint64_t cols) {
   Geom g;

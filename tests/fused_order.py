@@ -222,9 +222,9 @@ def fused_coefficient(orc, stream, v, policy="mixed"):
 # ---------------------------------------------------------------------------
 # tile-packed layout (k_pk_gemv, csrc/whff_packed.cu)
 # ---------------------------------------------------------------------------
-# * bands of 4 block-rows; a band's segments (256 block-columns) are dealt to
-#   32 virtual warps (segment s -> virtual warp s mod 32); within a segment
-#   tiles t = 0..7 of 32 block-columns, lane l = column 32 (8 s + t) + l;
+# * bands of 4 block-rows; a band's segments (SEG_TILES tiles of 32
+#   block-columns) are dealt to 32 virtual warps (segment s -> virtual warp
+#   s mod 32); lane l of tile t of segment s = column 32 (SEG_TILES s + t) + l;
 # * lane accumulators per (band row i, row r) add, per block, the
 #   coefficient-domain term binary32(w_r * 2^k) (w as fused_coefficient,
 #   every coefficient applied, q exact or rounded for |q| >= 2^24) or the
@@ -235,6 +235,9 @@ def fused_coefficient(orc, stream, v, policy="mixed"):
 # * lane butterfly, virtual-warp butterfly; y = binary32(R + sum_a G D_a) in
 #   the coefficient domain (fma order a = 0..3 onto R), binary32(D + R)
 #   exactly.
+
+SEG_TILES = 16   # csrc/whff_packed.cuh kSegTiles (tests/test_fused_order_model.py checks)
+
 
 def _exceptions(emax, raw):
     k = emax.astype(np.int64) - EMAX_BIAS - QUANT_BITS
@@ -254,8 +257,8 @@ def packed_model(orc, stream, v, policy="mixed", evaluation="coefficient"):
     bc, br = (cols + 3) // 4, (rows + 3) // 4
     nband = (br + 3) // 4
     ntile = (bc + 31) // 32
-    nsegb = (ntile + 7) // 8
-    nbp = nsegb * 256
+    nsegb = (ntile + SEG_TILES - 1) // SEG_TILES
+    nbp = nsegb * SEG_TILES * 32
     single = policy == "single"
     acc_t = np.float32 if single else np.float64
     vp = np.zeros(nbp * 4, np.float32)
@@ -311,8 +314,8 @@ def packed_model(orc, stream, v, policy="mixed", evaluation="coefficient"):
             for sb in range(vw, nsegb, 32):
                 Sg = np.zeros((32, 4, 4), np.float32)          # [lane, i, r] (coefficient)
                 Se = np.zeros((32, 4, 4), acc_t)               # [lane, i, r] (exact)
-                for tt in range(8):
-                    cs = (8 * sb + tt) * 32 + np.arange(32)
+                for tt in range(SEG_TILES):
+                    cs = (SEG_TILES * sb + tt) * 32 + np.arange(32)
                     for i in range(4):
                         b = 4 * band + i
                         if evaluation == "coefficient":
@@ -329,11 +332,11 @@ def packed_model(orc, stream, v, policy="mixed", evaluation="coefficient"):
                     Dv_acc[vw] = Dv_acc[vw] + _butterfly(np.moveaxis(Dseg, 0, -1)).astype(acc_t)
                 else:
                     Dv_acc[vw] = Dv_acc[vw] + _butterfly(np.moveaxis(Se.reshape(32, 16), 0, -1))
-                for tt in range(8):
+                for tt in range(SEG_TILES):
                     for i in range(4):
                         b = 4 * band + i
                         for lane in range(32):
-                            col = (8 * sb + tt) * 32 + lane
+                            col = (SEG_TILES * sb + tt) * 32 + lane
                             if col >= bc or b >= br or not exc[b, col]:
                                 continue
                             for r in range(4):

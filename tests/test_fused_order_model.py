@@ -44,3 +44,13 @@ def test_coefficient_model_within_reference_bound_smooth(orc, rng):
         ref = np.asarray(orc.gemv_kernel(words, v, "mixed", "sequential"), np.float64)
         bound = (C.shape[1] + 1) * np.finfo(np.float32).eps * (np.abs(words).astype(np.float64) @ v)
         assert (np.abs(got - ref) <= bound).all()
+
+
+def test_model_segment_size_matches_the_layout():
+    """fused_order.SEG_TILES restates csrc/whff_packed.cuh kSegTiles."""
+    import os
+    import re
+    from conftest import ROOT
+    from fused_order import SEG_TILES
+    hdr = open(os.path.join(ROOT, "paper_1902_08018_b200", "csrc", "whff_packed.cuh")).read()
+    assert int(re.search(r"#define WHFF_SEG_TILES (\d+)", hdr).group(1)) == SEG_TILES

@@ -236,8 +236,8 @@ def test_packed_rebind_drops_copy(rng):
 
 @pytest.mark.parametrize("policy", ["mixed", "single"])
 def test_staged_kernel_wide_bands(orc, policy, rng):
-    """More than 32 segments per virtual warp (cols > 1,048,576: the staged
-    kernel's header ring wraps) and row ranges: bit-exact vs the CPU model."""
+    """Over 16 segments per virtual warp (1.1 M columns: the staged kernel's
+    16-entry header ring wraps): bit-exact vs the CPU model."""
     from fused_order import packed_model
     from paper_1902_08018_b200 import codec
     C0 = smooth_matrix(9, 1_100_003, S=1_100_003)
@@ -254,9 +254,9 @@ def test_staged_kernel_runs_of_generic_segments(orc, evaluation, rng):
     wide for the fast path) between fast ones: the producer skips far ahead
     of the consumer through the header ring.  Every virtual warp sees a fast
     segment, 18 generic ones, then fast ones again; bit-exact vs the model."""
-    from fused_order import packed_model
+    from fused_order import SEG_TILES, packed_model
     from paper_1902_08018_b200 import codec
-    seg_cols, vws = 1024, 32
+    seg_cols, vws = 4 * 32 * SEG_TILES, 32
     cols = 20 * vws * seg_cols
     C0 = smooth_matrix(6, cols, S=cols)
     wild = rng.standard_normal((6, 18 * vws * seg_cols)).astype(np.float32) * np.float32(1e-8)

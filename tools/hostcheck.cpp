@@ -300,7 +300,7 @@ int64_t hc_pack(const uint32_t* mag, const uint8_t* neg, const uint16_t* emax, c
     for (int tt = 0; tt < ntl; ++tt)
       for (int i = 0; i < nrows; ++i)
         for (int lane = 0; lane < 32; ++lane) {
-          const uint64_t col = (sb * 8 + tt) * 32 + lane;
+          const uint64_t col = (sb * pk::kSegTiles + tt) * pk::kTile + lane;
           const uint64_t b = (band * 4 + i) * g.bc + col;
           int32_t q[16] = {0};
           uint32_t ed = 0;
@@ -362,7 +362,7 @@ int64_t hc_unpack(const uint8_t* segs_in, const uint32_t* body, const uint64_t* 
     for (int tt = 0; tt < pk::seg_tiles(g, sb); ++tt)
       for (int i = 0; i < nrows; ++i)
         for (int lane = 0; lane < 32; ++lane) {
-          const uint64_t col = (sb * 8 + tt) * 32 + lane;
+          const uint64_t col = (sb * pk::kSegTiles + tt) * pk::kTile + lane;
           if (col >= g.bc) continue;
           const uint32_t* tp = body + S.body + tt * TW;
           uint32_t rec[pk::kMaxRecordWords + 1] = {0};
