@@ -1343,7 +1343,7 @@ void drop_packed(whff_dstream* s) {
 
 PkView pk_view(const whff_dstream* s) {
   PkView v;
-  v.g = pk::make_geom(s->rows, s->cols);
+  v.g = pk::make_geom(s->rows, s->cols, pk::seg_tiles_for_mode(s->mode));
   v.body = s->d_pk_body;
   v.segs = s->d_pk_segs;
   v.pars = s->d_pk_segs ? reinterpret_cast<const pk::FieldPar*>(s->d_pk_segs + v.g.nband * v.g.nsegb) : nullptr;
@@ -1548,7 +1548,7 @@ whff_status_t whff_dstream_pack(whff_dstream_t s, whff_stream_t stream) {
   if (s->packed) return WHFF_OK;
   DeviceGuard g(s->device);
   cudaStream_t cs = (cudaStream_t)stream;
-  const pk::Geom gg = pk::make_geom(s->rows, s->cols);
+  const pk::Geom gg = pk::make_geom(s->rows, s->cols, pk::seg_tiles_for_mode(s->mode));
   const uint64_t nseg = gg.nband * gg.nsegb;
   pk::Seg* segs = nullptr;
   uint64_t *words = nullptr, *exc = nullptr, *off = nullptr, *eoff = nullptr;
@@ -1628,7 +1628,7 @@ whff_status_t whff_dstream_packed_download(whff_dstream_t s, uint8_t* segs, uint
                                            uint64_t* n_exc) {
   if (!s) return fail(WHFF_ERR_ARGUMENT, "null stream");
   if (!s->packed) return fail(WHFF_ERR_ARGUMENT, "stream is not packed (whff_dstream_pack)");
-  const pk::Geom gg = pk::make_geom(s->rows, s->cols);
+  const pk::Geom gg = pk::make_geom(s->rows, s->cols, pk::seg_tiles_for_mode(s->mode));
   const uint64_t nseg = gg.nband * gg.nsegb;
   if (n_segs) *n_segs = nseg;
   if (body_words) *body_words = s->pk_body_words;
@@ -1669,7 +1669,7 @@ whff_status_t whff_dstream_clone(whff_dstream_t s, whff_dstream_t* out) {
     if (e == cudaSuccess) e = cudaMemcpy(c->d_starts, s->d_starts, s->nb * 8, cudaMemcpyDeviceToDevice);
   }
   if (e == cudaSuccess && s->packed) {
-    const pk::Geom gg = pk::make_geom(s->rows, s->cols);
+    const pk::Geom gg = pk::make_geom(s->rows, s->cols, pk::seg_tiles_for_mode(s->mode));
     const uint64_t nseg = gg.nband * gg.nsegb;
     e = cudaMalloc(&c->d_pk_body, s->pk_alloc_words * 4);
     if (e == cudaSuccess)
@@ -1715,7 +1715,7 @@ whff_status_t whff_dstream_get_info(whff_dstream_t s, whff_dstream_info_t* info)
   info->device = s->device;
   info->packed_exceptions = s->pk_nexc;
   if (s->packed) {
-    const pk::Geom gg = pk::make_geom(s->rows, s->cols);
+    const pk::Geom gg = pk::make_geom(s->rows, s->cols, pk::seg_tiles_for_mode(s->mode));
     info->packed_bytes = s->pk_body_words * 4 + pk_segs_bytes(gg.nband * gg.nsegb) + s->pk_nexc * 72;
     info->device_bytes += s->pk_alloc_words * 4 + pk_segs_bytes(gg.nband * gg.nsegb) +
                           std::max<uint64_t>(s->pk_nexc, 1) * 72;

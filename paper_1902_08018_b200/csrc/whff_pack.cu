@@ -24,8 +24,8 @@ __global__ void __launch_bounds__(256) k_pk_stats(StreamView s, pk::Geom g, pk::
   if (sid >= g.nband * g.nsegb) return;
   const uint64_t band = sid / g.nsegb, sb = sid % g.nsegb;
   const int nrows = pk::band_rows(g, band);
-  const uint64_t col0 = sb * pk::kSegCols;
-  const uint64_t ncols = min((uint64_t)pk::kSegCols, g.bc - col0);
+  const uint64_t col0 = sb * g.segt * pk::kTile;
+  const uint64_t ncols = min(g.segt * pk::kTile, g.bc - col0);
   uint32_t wmax[16];
 #pragma unroll
   for (int c = 0; c < 16; ++c) wmax[c] = 0;
@@ -117,7 +117,7 @@ __global__ void __launch_bounds__(256) k_pk_emit(StreamView s, pk::Geom g, const
   uint64_t exc = S.exc_begin;
   const int ntl = pk::seg_tiles(g, sb);
   for (int tt = 0; tt < ntl; ++tt) {
-    const uint64_t col = (sb * pk::kSegTiles + tt) * pk::kTile + lane;
+    const uint64_t col = (sb * g.segt + tt) * pk::kTile + lane;
     const bool active = col < g.bc;
     for (int i = 0; i < nrows; ++i) {
       const uint64_t b = (band * pk::kBand + i) * g.bc + col;

@@ -300,7 +300,7 @@ struct alignas(16) P2Ctl {
   uint64_t pbody, usrc;                  // next item: body and U source addresses
   uint32_t pk, pt, pntl, pslot;          // producer cursor: segment, tile, its tiles, stage
   uint32_t ptw, nseg, hdr_loaded, ntile; // words per tile of segment pk; warp constants
-  uint32_t hdr_landed, pad0, pad1, pad2;  // header ring: slots known to have landed
+  uint32_t hdr_landed, segt, pad1, pad2;  // header ring: slots known to have landed; tiles per segment
   uint64_t body, U, gsegs, gpars, policy, pad;
 };
 template <typename AT>
@@ -729,6 +729,7 @@ __global__ void __launch_bounds__(32 * kP2Warps, WHFF_P2_MINB) k_pk_gemv2(PkTabl
   const uint32_t c_pslot = ctl + offsetof(P2Ctl, pslot), c_pntl = ctl + offsetof(P2Ctl, pntl);
   const uint32_t c_nseg = ctl + offsetof(P2Ctl, nseg), c_hdr = ctl + offsetof(P2Ctl, hdr_loaded);
   const uint32_t c_ntile = ctl + offsetof(P2Ctl, ntile), c_landed = ctl + offsetof(P2Ctl, hdr_landed);
+  const uint32_t c_segt = ctl + offsetof(P2Ctl, segt);
   {
     const PkView& P = J.p;
     const uint64_t nsegb = P.g.nsegb;
@@ -747,6 +748,7 @@ __global__ void __launch_bounds__(32 * kP2Warps, WHFF_P2_MINB) k_pk_gemv2(PkTabl
       ctl_st32(c_nseg, (uint32_t)nseg);
       ctl_st32(c_hdr, 0);
       ctl_st32(c_landed, 0);
+      ctl_st32(c_segt, (uint32_t)P.g.segt);
       ctl_st32(c_ntile, (uint32_t)P.g.ntile);
     }
     if (lane < 16) W.rs[lane] = (AT)0;
@@ -801,8 +803,9 @@ __global__ void __launch_bounds__(32 * kP2Warps, WHFF_P2_MINB) k_pk_gemv2(PkTabl
   auto hdr = [&](int k) -> const pk::Seg& { return W.seg[k & (kP2HdrRing - 1)]; };
   auto seg_ntl = [&](int k) -> int {   // tiles of the warp's segment k
     const uint64_t ntile = ctl_ld32(c_ntile);
-    const uint64_t t0 = (vw + (uint64_t)kVW * k) * pk::kSegTiles;
-    return ntile - t0 < (uint64_t)pk::kSegTiles ? (int)(ntile - t0) : pk::kSegTiles;
+    const uint64_t segt = ctl_ld32(c_segt);
+    const uint64_t t0 = (vw + (uint64_t)kVW * k) * segt;
+    return ntile - t0 < segt ? (int)(ntile - t0) : (int)segt;
   };
   // producer: the cursor is warp-uniform and lives in W.ctl; lane 0 issues.
   // skip(): from (pk, pt) to the next tile of a fast segment (or the end)
@@ -815,7 +818,7 @@ __global__ void __launch_bounds__(32 * kP2Warps, WHFF_P2_MINB) k_pk_gemv2(PkTabl
       if (!pk::seg_generic(S) && pt < ntl) {
         if (lane == 0) {
           const uint32_t tw = (uint32_t)pk::tile_words(pk::seg_L(S));
-          const uint64_t col0 = ((vw + (uint64_t)kVW * pk) * pk::kSegTiles + pt) * pk::kTile;
+          const uint64_t col0 = ((vw + (uint64_t)kVW * pk) * ctl_ld32(c_segt) + pt) * pk::kTile;
           const uint64_t pbody = ctl_ld64(c_body) + 4 * (S.body + (uint64_t)pt * tw);
           const uint64_t usrc = ctl_ld64(c_U) + col0 * 16;
           ctl_st128(c_A, make_uint4((uint32_t)pbody, (uint32_t)(pbody >> 32), (uint32_t)usrc,
@@ -987,7 +990,7 @@ __global__ void __launch_bounds__(32 * kP2Warps, WHFF_P2_MINB) k_pk_gemv2(PkTabl
       const uint32_t* sbody = P.body + S.body;
       const uint64_t sb = vw + (uint64_t)kVW * k;
       for (int tt = 0; tt < ntl; ++tt) {
-        const uint64_t col = (sb * pk::kSegTiles + tt) * pk::kTile + lane;
+        const uint64_t col = (sb * P.g.segt + tt) * pk::kTile + lane;
         if (col >= P.g.bc) continue;
         const float4 u4 = ldg(J.U + col);
         const float u[4] = {u4.x, u4.y, u4.z, u4.w};
@@ -1078,8 +1081,8 @@ __global__ void __launch_bounds__(256) k_pk_words(PkView P, float* out, uint64_t
   const int warp = threadIdx.x >> 5;
   if (wid >= P.g.nband * P.g.ntile) return;
   const uint64_t band = wid / P.g.ntile, t = wid % P.g.ntile;
-  const uint64_t sb = t / pk::kSegTiles;
-  const int tt = (int)(t % pk::kSegTiles);
+  const uint64_t sb = t / P.g.segt;
+  const int tt = (int)(t % P.g.segt);
   const int nrows = pk::band_rows(P.g, band);
   const pk::Seg S = P.segs[band * P.g.nsegb + sb];
   const int L = pk::seg_L(S), R = pk::rec_words(L), We = pk::seg_We(S);

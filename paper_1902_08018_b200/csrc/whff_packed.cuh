@@ -14,7 +14,7 @@
 //   band     = 4 block-rows (16 matrix rows)
 //   tile     = band x 32 block-columns; lane l of a warp owns block-column
 //              32 t + l of every block-row of the band
-//   segment  = band x up to 16 tiles (512 block-columns) sharing one "field
+//   segment  = band x up to 8 or 16 tiles (per stream) sharing one "field
 //              profile": a width W_c per coefficient c (sequency order,
 //              codec.py:40) = the widest value of c in the segment, and a
 //              width W_e for emax - emax_base
@@ -57,11 +57,14 @@ namespace pk {
 
 constexpr int kBand = 4;          // block-rows per band
 constexpr int kTile = 32;         // block-columns per tile (one per lane)
-#ifndef WHFF_SEG_TILES
-#define WHFF_SEG_TILES 16
-#endif
-constexpr int kSegTiles = WHFF_SEG_TILES;   // tiles per segment (tests/fused_order.py SEG_TILES)
-constexpr int kSegCols = kTile * kSegTiles;
+// Tiles per segment, chosen per stream at pack time (seg_tiles_for_mode):
+// 16 for the variable-rate modes (short records: per-segment control is a
+// large share, and the field widths barely grow), 8 for FixedRate (longer
+// segments widen its fields enough to cost more than they save).
+constexpr int kSegTilesRate = 8;
+constexpr int kSegTilesVar = 16;
+constexpr int kSegTiles = kSegTilesVar;   // the largest (tests/fused_order.py seg_tiles_for)
+WHFF_HD int seg_tiles_for_mode(int mode) { return mode == 0 ? kSegTilesRate : kSegTilesVar; }
 constexpr int kMagicW = 23;       // widest offset-binary field on the magic path
 constexpr int kMaxRecordBits = 9 + 28 * 16;
 constexpr int kMaxRecordWords = (kMaxRecordBits + 31) / 32;   // 15
@@ -195,17 +198,19 @@ struct Geom {
   uint64_t rows, cols, br, bc;
   uint64_t nband;   // ceil(br / 4)
   uint64_t ntile;   // tiles per band: ceil(bc / 32)
-  uint64_t nsegb;   // segments per band: ceil(ntile / kSegTiles)
+  uint64_t nsegb;   // segments per band: ceil(ntile / segt)
+  uint64_t segt;    // tiles per segment
 };
-WHFF_HD Geom make_geom(uint64_t rows, uint64_t cols) {
+WHFF_HD Geom make_geom(uint64_t rows, uint64_t cols, int segt) {
   Geom g;
+  g.segt = (uint64_t)segt;
   g.rows = rows;
   g.cols = cols;
   g.br = (rows + 3) / 4;
   g.bc = (cols + 3) / 4;
   g.nband = (g.br + kBand - 1) / kBand;
   g.ntile = (g.bc + kTile - 1) / kTile;
-  g.nsegb = (g.ntile + kSegTiles - 1) / kSegTiles;
+  g.nsegb = (g.ntile + g.segt - 1) / g.segt;
   return g;
 }
 WHFF_HD int band_rows(const Geom& g, uint64_t band) {
@@ -213,8 +218,8 @@ WHFF_HD int band_rows(const Geom& g, uint64_t band) {
   return r < (uint64_t)kBand ? (int)r : kBand;
 }
 WHFF_HD int seg_tiles(const Geom& g, uint64_t sb) {
-  const uint64_t r = g.ntile - sb * kSegTiles;
-  return r < (uint64_t)kSegTiles ? (int)r : kSegTiles;
+  const uint64_t r = g.ntile - sb * g.segt;
+  return r < g.segt ? (int)r : (int)g.segt;
 }
 
 // record bits: put the low W bits of val at record bits [pos, pos + W)

@@ -61,9 +61,9 @@ def hostcheck():
     L.hc_encode_blocks.restype = i64
     L.hc_relayout.argtypes = [p, p, p, p, i64, u64, ci, ci, ci]
     L.hc_decode_blocks_sf.argtypes = [p, u64, p, p, i64, ci, ci] + [p] * 6
-    L.hc_pack.argtypes = [p] * 5 + [i64, i64] + [p] * 7
+    L.hc_pack.argtypes = [p] * 5 + [i64, i64] + [p] * 7 + [ci]
     L.hc_pack.restype = i64
-    L.hc_unpack.argtypes = [p, p, p, p, i64, i64, i64, p]
+    L.hc_unpack.argtypes = [p, p, p, p, i64, i64, i64, p, ci]
     L.hc_unpack.restype = i64
     return L
 

@@ -223,7 +223,8 @@ def fused_coefficient(orc, stream, v, policy="mixed"):
 # tile-packed layout (k_pk_gemv, csrc/whff_packed.cu)
 # ---------------------------------------------------------------------------
 # * bands of 4 block-rows; a band's segments (SEG_TILES tiles of 32
-#   block-columns) are dealt to 32 virtual warps (segment s -> virtual warp
+#   block-columns, per stream mode: packed_host.seg_tiles_for) are dealt to
+#   32 virtual warps (segment s -> virtual warp
 #   s mod 32); lane l of tile t of segment s = column 32 (SEG_TILES s + t) + l;
 # * lane accumulators per (band row i, row r) add, per block, the
 #   coefficient-domain term binary32(w_r * 2^k) (w as fused_coefficient,
@@ -235,9 +236,6 @@ def fused_coefficient(orc, stream, v, policy="mixed"):
 # * lane butterfly, virtual-warp butterfly; y = binary32(R + sum_a G D_a) in
 #   the coefficient domain (fma order a = 0..3 onto R), binary32(D + R)
 #   exactly.
-
-SEG_TILES = 16   # csrc/whff_packed.cuh kSegTiles (tests/test_fused_order_model.py checks)
-
 
 def _exceptions(emax, raw):
     k = emax.astype(np.int64) - EMAX_BIAS - QUANT_BITS
@@ -257,6 +255,8 @@ def packed_model(orc, stream, v, policy="mixed", evaluation="coefficient"):
     bc, br = (cols + 3) // 4, (rows + 3) // 4
     nband = (br + 3) // 4
     ntile = (bc + 31) // 32
+    from packed_host import seg_tiles_for
+    SEG_TILES = seg_tiles_for(stream.mode)
     nsegb = (ntile + SEG_TILES - 1) // SEG_TILES
     nbp = nsegb * SEG_TILES * 32
     single = policy == "single"

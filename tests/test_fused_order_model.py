@@ -47,10 +47,12 @@ def test_coefficient_model_within_reference_bound_smooth(orc, rng):
 
 
 def test_model_segment_size_matches_the_layout():
-    """fused_order.SEG_TILES restates csrc/whff_packed.cuh kSegTiles."""
+    """packed_host.seg_tiles_for restates csrc/whff_packed.cuh seg_tiles_for_mode."""
     import os
     import re
     from conftest import ROOT
-    from fused_order import SEG_TILES
+    from packed_host import seg_tiles_for
     hdr = open(os.path.join(ROOT, "paper_1902_08018_b200", "csrc", "whff_packed.cuh")).read()
-    assert int(re.search(r"#define WHFF_SEG_TILES (\d+)", hdr).group(1)) == SEG_TILES
+    assert int(re.search(r"kSegTilesRate = (\d+);", hdr).group(1)) == seg_tiles_for("rate")
+    assert int(re.search(r"kSegTilesVar = (\d+);", hdr).group(1)) == seg_tiles_for("accuracy")
+    assert seg_tiles_for("precision") == seg_tiles_for("accuracy")

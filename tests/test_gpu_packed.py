@@ -53,7 +53,7 @@ def test_device_packer_matches_host_packer_on_goldens(golden, hostcheck):
             continue
         s = host_stream(case)
         mag, neg, emax, raw, raw_words, _ = case["dec"]
-        hp = ph.pack(hostcheck, mag, neg, emax, raw, raw_words, s.rows, s.cols)
+        hp = ph.pack(hostcheck, mag, neg, emax, raw, raw_words, s.rows, s.cols, s.mode)
         ds = codec.DeviceStream.from_host(s).pack()
         assert ds.packed and ds.packed_exceptions == hp["exc_block"].size
         segs, body, xb, xw = download_packed(ds)
@@ -254,9 +254,9 @@ def test_staged_kernel_runs_of_generic_segments(orc, evaluation, rng):
     wide for the fast path) between fast ones: the producer skips far ahead
     of the consumer through the header ring.  Every virtual warp sees a fast
     segment, 18 generic ones, then fast ones again; bit-exact vs the model."""
-    from fused_order import SEG_TILES, packed_model
+    from fused_order import packed_model
     from paper_1902_08018_b200 import codec
-    seg_cols, vws = 4 * 32 * SEG_TILES, 32
+    seg_cols, vws = 4 * 32 * ph.seg_tiles_for("rate"), 32
     cols = 20 * vws * seg_cols
     C0 = smooth_matrix(6, cols, S=cols)
     wild = rng.standard_normal((6, 18 * vws * seg_cols)).astype(np.float32) * np.float32(1e-8)

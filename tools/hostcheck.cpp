@@ -248,21 +248,22 @@ whff::Decoded hs_block(const HostStream& h, uint64_t b) {
 
 extern "C" {
 
-// Pack (mag, neg, emax, raw, raw_words) of a rows x cols stream.  Pass NULL
+// Pack (mag, neg, emax, raw, raw_words) of a rows x cols stream of codec
+// mode `mode` (0 rate, 1 precision, 2 accuracy: the segment size).  Pass NULL
 // outputs to size: returns body words; *nseg_out, *nexc_out.
 int64_t hc_pack(const uint32_t* mag, const uint8_t* neg, const uint16_t* emax, const uint8_t* raw,
                 const uint32_t* raw_words, int64_t rows, int64_t cols, uint8_t* segs_out,
                 uint32_t* body_out, uint64_t* exc_block_out, uint32_t* exc_words_out,
-                int64_t* nseg_out, int64_t* nexc_out, int64_t* generic_out) {
+                int64_t* nseg_out, int64_t* nexc_out, int64_t* generic_out, int mode) {
   using namespace whff;
   const HostStream hs{mag, neg, emax, raw, raw_words};
-  const pk::Geom g = pk::make_geom(rows, cols);
+  const pk::Geom g = pk::make_geom(rows, cols, pk::seg_tiles_for_mode(mode));
   const uint64_t nseg = g.nband * g.nsegb;
   uint64_t body = 0, nexc = 0, generic = 0;
   for (uint64_t sid = 0; sid < nseg; ++sid) {
     const uint64_t band = sid / g.nsegb, sb = sid % g.nsegb;
     const int nrows = pk::band_rows(g, band);
-    const uint64_t col0 = sb * pk::kSegCols, ncols = std::min<uint64_t>(pk::kSegCols, g.bc - col0);
+    const uint64_t col0 = sb * g.segt * pk::kTile, ncols = std::min<uint64_t>(g.segt * pk::kTile, g.bc - col0);
     int W[16] = {0};
     uint32_t emin = 0xFFFF, emx = 0, ne = 0;
     for (int i = 0; i < nrows; ++i)
@@ -300,7 +301,7 @@ int64_t hc_pack(const uint32_t* mag, const uint8_t* neg, const uint16_t* emax, c
     for (int tt = 0; tt < ntl; ++tt)
       for (int i = 0; i < nrows; ++i)
         for (int lane = 0; lane < 32; ++lane) {
-          const uint64_t col = (sb * pk::kSegTiles + tt) * pk::kTile + lane;
+          const uint64_t col = (sb * g.segt + tt) * pk::kTile + lane;
           const uint64_t b = (band * 4 + i) * g.bc + col;
           int32_t q[16] = {0};
           uint32_t ed = 0;
@@ -342,9 +343,9 @@ int64_t hc_pack(const uint32_t* mag, const uint8_t* neg, const uint16_t* emax, c
 // kernels' extraction (fields_int) and checked against parse_record.
 // Returns the number of records where the two disagree.
 int64_t hc_unpack(const uint8_t* segs_in, const uint32_t* body, const uint64_t* exc_block,
-                  const uint32_t* exc_words, int64_t nexc, int64_t rows, int64_t cols, float* out) {
+                  const uint32_t* exc_words, int64_t nexc, int64_t rows, int64_t cols, float* out, int mode) {
   using namespace whff;
-  const pk::Geom g = pk::make_geom(rows, cols);
+  const pk::Geom g = pk::make_geom(rows, cols, pk::seg_tiles_for_mode(mode));
   int64_t bad = 0;
   for (uint64_t sid = 0; sid < g.nband * g.nsegb; ++sid) {
     pk::Seg S;
@@ -362,7 +363,7 @@ int64_t hc_unpack(const uint8_t* segs_in, const uint32_t* body, const uint64_t* 
     for (int tt = 0; tt < pk::seg_tiles(g, sb); ++tt)
       for (int i = 0; i < nrows; ++i)
         for (int lane = 0; lane < 32; ++lane) {
-          const uint64_t col = (sb * pk::kSegTiles + tt) * pk::kTile + lane;
+          const uint64_t col = (sb * g.segt + tt) * pk::kTile + lane;
           if (col >= g.bc) continue;
           const uint32_t* tp = body + S.body + tt * TW;
           uint32_t rec[pk::kMaxRecordWords + 1] = {0};
