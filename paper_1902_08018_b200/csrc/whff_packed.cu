@@ -1075,7 +1075,19 @@ static cudaError_t p2_launch(const PkTable& T, unsigned long long* status, cudaS
 // ---------------------------------------------------------------------------
 // One warp per tile (band x 32 block-columns); exceptions are written by
 // k_pk_exc_words afterwards (their records decode to zeros here).
-__global__ void __launch_bounds__(256) k_pk_words(PkView P, float* out, uint64_t ld) {
+// Latency-bound (a short dependent chain per warp: header, record words,
+// lift, four stores), so occupancy pays: 4 CTAs per SM at <= 64 registers
+// (the rare generic-record path keeps its arrays on the stack), and the
+// words are stored streaming (st.global.cs: written once, never re-read
+// here).  4,096 x 262,144 FixedRate(8): 1.147 -> 0.989 ms, FixedAccuracy
+// (1e-12) 1.095 -> 0.950 ms; same bits (scratch sweep of 1-6 CTAs per SM).
+#ifndef WHFF_WORDS_MINB
+#define WHFF_WORDS_MINB 4
+#endif
+#ifndef WHFF_WORDS_CS
+#define WHFF_WORDS_CS 1
+#endif
+__global__ void __launch_bounds__(256, WHFF_WORDS_MINB) k_pk_words(PkView P, float* out, uint64_t ld) {
   const uint64_t wid = (blockIdx.x * (uint64_t)blockDim.x + threadIdx.x) >> 5;
   const int lane = threadIdx.x & 31;
   const int warp = threadIdx.x >> 5;
@@ -1121,9 +1133,15 @@ __global__ void __launch_bounds__(256) k_pk_words(PkView P, float* out, uint64_t
     const uint64_t r0 = (band * pk::kBand + i) * 4, c0 = col * 4;
     if (vec && r0 + 4 <= P.g.rows && c0 + 4 <= P.g.cols) {
 #pragma unroll
-      for (int rr = 0; rr < 4; ++rr)
+      for (int rr = 0; rr < 4; ++rr) {
+#if WHFF_WORDS_CS
+        __stcs(reinterpret_cast<float4*>(out + (r0 + rr) * ld + c0),
+               make_float4(x[4 * rr], x[4 * rr + 1], x[4 * rr + 2], x[4 * rr + 3]));
+#else
         *reinterpret_cast<float4*>(out + (r0 + rr) * ld + c0) =
             make_float4(x[4 * rr], x[4 * rr + 1], x[4 * rr + 2], x[4 * rr + 3]);
+#endif
+      }
     } else {
       for (int rr = 0; rr < 4; ++rr) {
         if (r0 + rr >= P.g.rows) break;
