@@ -1162,22 +1162,35 @@ __global__ void __launch_bounds__(128) k_relayout(StreamView s, const uint32_t* 
 // ---------------------------------------------------------------------------
 // GPU encoder (codec.py:225-293, K:139-283)
 // ---------------------------------------------------------------------------
-__global__ void k_encode_len(const float* a, uint64_t lda, uint64_t rows, uint64_t cols, uint64_t nb,
-                             uint64_t bc, int mode, double param, uint64_t* lens, int* overflow) {
+// One thread per block, a long dependent chain (transform, plane search,
+// bit-plane emission) and little memory traffic: occupancy hides it, so both
+// passes are held to 64 registers (8 CTAs of 128 per SM).  Paper slit
+// (378 x 256,000): FixedRate(8) 10.4 -> 5.6 ms (also: no counting pass at a
+// fixed rate), FixedAccuracy(1e-12) 7.1 -> 6.0 ms, FixedPrecision(17) 6.1 ->
+// 4.5 ms; byte-identical streams (scratch sweep of 1, 6, 8 CTAs per SM).
+#ifndef WHFF_ENC_MINB
+#define WHFF_ENC_MINB 8
+#endif
+__global__ void __launch_bounds__(128, WHFF_ENC_MINB) k_encode_len(const float* a, uint64_t lda, uint64_t rows,
+                                                                  uint64_t cols, uint64_t nb, uint64_t bc, int mode,
+                                                                  double param, uint64_t* lens, int* overflow) {
   const uint64_t b = blockIdx.x * (uint64_t)blockDim.x + threadIdx.x;
   if (b >= nb) return;
   BlockPlan pl;
   plan_block(a, (int64_t)lda, (int64_t)rows, (int64_t)cols, (int64_t)b, (int64_t)bc, mode, param, pl);
   if (!pl.ok) atomicOr(overflow, 1);
   const int budget = mode == WHFF_MODE_RATE ? (int)param * 16 : 0;
-  CountSink cs;
-  int n = encode_one(pl.mag, pl.negm, pl.code, pl.planes, pl.raw, pl.raw_words, budget,
-                     mode == WHFF_MODE_ACCURACY, cs);
-  if (budget) n = budget;
+  // FixedRate: every block takes exactly its budget (codec.py:268-272, the
+  // stream pads short blocks), so there is nothing to count
+  int n = budget;
+  if (!budget) {
+    CountSink cs;
+    n = encode_one(pl.mag, pl.negm, pl.code, pl.planes, pl.raw, pl.raw_words, 0, mode == WHFF_MODE_ACCURACY, cs);
+  }
   lens[b] = (uint64_t)n;
 }
 
-__global__ void k_encode_emit(const float* a, uint64_t lda, uint64_t rows, uint64_t cols, uint64_t nb,
+__global__ void __launch_bounds__(128, WHFF_ENC_MINB) k_encode_emit(const float* a, uint64_t lda, uint64_t rows, uint64_t cols, uint64_t nb,
                               uint64_t bc, int mode, double param, const uint64_t* offsets,
                               uint32_t* words) {
   const uint64_t b = blockIdx.x * (uint64_t)blockDim.x + threadIdx.x;

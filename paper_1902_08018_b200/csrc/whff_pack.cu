@@ -17,7 +17,10 @@ static unsigned grid_of(uint64_t n, unsigned t) { return (unsigned)((n + t - 1) 
 // One warp per segment; lane-strided over the segment's blocks, each decoded
 // from the source stream with the general decoder (any layout, any index).
 template <bool HAS_RAW>
-__global__ void __launch_bounds__(256) k_pk_stats(StreamView s, pk::Geom g, pk::Seg* segs,
+#ifndef WHFF_PK_MINB
+#define WHFF_PK_MINB 1
+#endif
+__global__ void __launch_bounds__(256, WHFF_PK_MINB) k_pk_stats(StreamView s, pk::Geom g, pk::Seg* segs,
                                                   uint64_t* seg_words, uint64_t* seg_exc) {
   const uint64_t sid = (blockIdx.x * (uint64_t)blockDim.x + threadIdx.x) >> 5;
   const int lane = threadIdx.x & 31;
@@ -99,7 +102,7 @@ __device__ __forceinline__ void seg_layout(const pk::Seg& S, int W[16], pk::Layo
 // packer, pass 2: records and exceptions
 // ---------------------------------------------------------------------------
 template <bool HAS_RAW>
-__global__ void __launch_bounds__(256) k_pk_emit(StreamView s, pk::Geom g, const pk::Seg* segs,
+__global__ void __launch_bounds__(256, WHFF_PK_MINB) k_pk_emit(StreamView s, pk::Geom g, const pk::Seg* segs,
                                                  uint32_t* body, uint64_t* exc_block,
                                                  uint32_t* exc_words) {
   const uint64_t sid = (blockIdx.x * (uint64_t)blockDim.x + threadIdx.x) >> 5;
