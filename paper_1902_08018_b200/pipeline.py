@@ -70,7 +70,11 @@ class PipelineConfig:
     # B200 additions
     evaluation: str = "exact"                  # "reference" | "exact" | "coefficient"
     policy: str = "mixed"
-    layout: str = "skeleton-first"
+    layout: str = None                         # device layout of resident slits: "packed"
+                                               # (default: the tile-packed copy read by
+                                               # k_pk_gemv2), "skeleton-first", "reference";
+                                               # streaming stages a stream layout
+                                               # (default "skeleton-first")
     step_period_s: float = None                # pace steps on the device clock
     streaming: bool = False                    # stage 1 = H2D of the slit streams (ring of
                                                # queue_depth device slots)
@@ -90,6 +94,13 @@ class PipelineConfig:
             raise WhffError("step_period_s must be positive")
         if self.codec_mode is None:
             self.codec_mode = codec_mod.FixedAccuracy(1e-12)
+        if self.layout is None:
+            self.layout = "skeleton-first" if self.streaming else "packed"
+        if self.layout not in ("packed", "skeleton-first", "reference"):
+            raise WhffError(f"unknown layout {self.layout!r}")
+        if self.streaming and self.layout == "packed":
+            raise WhffError("streaming stages the stream layouts (skeleton-first or reference); "
+                            "the packed copy is built on the device for resident slits")
         if self.streaming and not self.use_compression:
             raise WhffError("streaming stages compressed slit streams (use_compression=True)")
 
@@ -161,7 +172,9 @@ class _Slit:
             if cfg.use_compression:
                 ds = codec_mod.compress_device(rows, cfg.codec_mode)
                 self.nbytes += ds.payload_bytes
-                if cfg.evaluation != "reference" and cfg.layout != "reference":
+                if cfg.layout == "packed":
+                    ds.pack()
+                elif cfg.evaluation != "reference" and cfg.layout != "reference":
                     ds.relayout(cfg.layout)
                 if cfg.streaming:
                     self.host.append(ds.export(pinned=True))

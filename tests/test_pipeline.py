@@ -108,3 +108,15 @@ def test_streaming_config_needs_compression():
         pipeline.PipelineConfig(streaming=True)              # nothing compressed to stage
     pipeline.PipelineConfig(streaming=True, use_compression=True)
     pipeline.PipelineConfig(streaming=True, use_compression=True, codec_mode=codec.FixedRate(8))
+
+
+def test_layout_defaults():
+    """Resident slits default to the tile-packed copy (the k_pk_gemv2 path);
+    streaming stages a stream layout (skeleton-first) and rejects packed."""
+    assert pipeline.PipelineConfig(use_compression=True).layout == "packed"
+    assert pipeline.PipelineConfig(streaming=True, use_compression=True).layout == "skeleton-first"
+    assert pipeline.PipelineConfig(layout="reference").layout == "reference"
+    with pytest.raises(WhffError):
+        pipeline.PipelineConfig(streaming=True, use_compression=True, layout="packed")
+    with pytest.raises(WhffError):
+        pipeline.PipelineConfig(layout="tiled")
