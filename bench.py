@@ -69,7 +69,7 @@ def parse():
                          "so the step needs no broadcast and stays CUDA-graph captured; "
                          "broadcast: rank 0 computes S and broadcasts it")
     ap.add_argument("--no-cpu-baseline", action="store_true")
-    ap.add_argument("--variants", default="exact,accuracy:1e-12",
+    ap.add_argument("--variants", default="exact,accuracy:1e-12,precision:17",
                     help="extra lines measured after the headline (N=1): 'exact' = the same "
                          "streams with the reference's products (exact evaluation); "
                          "'<mode>' = the same step over streams of another codec mode "
